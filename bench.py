@@ -1,0 +1,422 @@
+"""Benchmark: per-sentence BLEU-4 sentences/s at 512x1024 tokens (V=128k, R=1),
+BASELINE.json configs[1] — plus the HBM roofline of the fused kernel and the
+reference CPU path timed on this host.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A "step" is one pass of the hot path over one batch of the workload: the
+batch's per-sentence statistics and BLEU scores.  Multi-GPU is weak scaling:
+every rank scores its own 512x1024 batch (rows shard with no data-path
+collective), value = all sentences / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (B, L, V, R, smoothing)   — BASELINE.json configs
+    "c1": (16, 256, 32000, 1, "floor"),
+    "c2": (512, 1024, 128000, 1, "none"),
+    "c3": (256, 1024, 128000, 4, "add-k"),
+    "c4": (4096, 1024, 128000, 1, "none"),
+    "c5": (2048, 2048, 256000, 1, "none"),  # per-GPU shard of 16384x2048 over 8 GPUs
+}
+METRIC = "per-sentence BLEU-4 sentences/sec at 512x1024 tok; HBM roofline %; vs CPU ref"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def generate_batch(b, l, v, r, seed=42):
+    """The reference generator, bench.py:72-91: default_rng([seed, B, L, V]),
+    IDs uniform in [0, V), lengths uniform in [L/2, L]; candidates then refs."""
+    rng = np.random.default_rng([seed, b, l, v])
+
+    def draw():
+        ids = rng.integers(0, v, size=(b, l), dtype=np.int64)
+        lengths = rng.integers(l // 2, l + 1, size=b, dtype=np.int64)
+        return ids, lengths
+
+    cand = draw()
+    return cand, [draw() for _ in range(r)]
+
+
+def algorithmic_bytes(lengths_rows, v, b, max_order=4):
+    """A = 4·Σ len + Σ_n T_n·(2·s_k(n) + 8) + 8·B."""
+    lens = np.concatenate([np.asarray(x, dtype=np.int64) for x in lengths_rows])
+    bits = math.ceil(math.log2(v))
+    a = 4 * int(lens.sum()) + 8 * b
+    for n in range(1, max_order + 1):
+        t_n = int(np.maximum(lens - n + 1, 0).sum())
+        s_k = 8 if n * bits <= 64 else 16
+        a += t_n * (2 * s_k + 8)
+    return a
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (reference package from oracle/_ref, else the C oracle port)
+# ---------------------------------------------------------------------------
+def _ref_pkg():
+    import oracle
+    return oracle.reference_package()
+
+
+def cpu_reference_single(cand, refs, smoothing, repeats=3):
+    """The reference's shipped path: batchbleu.sentence_bleu, compiled backend,
+    threads=1 — 1 warm-up + `repeats` timed runs over the whole batch."""
+    bb = _ref_pkg()
+    if bb is not None:
+        c = bb.TokenBatch(ids=cand[0], lengths=cand[1])
+        rs = [bb.TokenBatch(ids=i, lengths=l) for i, l in refs]
+        cfg = bb.BleuConfig(smoothing=smoothing)
+        bb.sentence_bleu(c, rs, cfg)
+        ts = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            bb.sentence_bleu(c, rs, cfg)
+            ts.append(time.perf_counter() - t0)
+        return min(ts), "reference", "batchbleu.sentence_bleu (oracle/_ref, compiled backend, threads=1)"
+    import oracle
+    oracle.stats(cand[0][:8], cand[1][:8], [(i[:8], l[:8]) for i, l in refs])
+    ts = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        st = oracle.stats(cand[0], cand[1], refs)
+        oracle.scores(st, smoothing)
+        ts.append(time.perf_counter() - t0)
+    return min(ts), "port", "oracle/tbleu_oracle.c (C restatement, 1 thread)"
+
+
+_POOL_DATA = {}
+
+
+def _pool_init(cand, refs, smoothing):
+    _POOL_DATA.update(cand=cand, refs=refs, smoothing=smoothing)
+    import oracle
+    oracle.reference_package()
+
+
+def _pool_work(span):
+    import batchbleu as bb
+    lo, hi = span
+    cand, refs = _POOL_DATA["cand"], _POOL_DATA["refs"]
+    c = bb.TokenBatch(ids=cand[0][lo:hi], lengths=cand[1][lo:hi])
+    rs = [bb.TokenBatch(ids=i[lo:hi], lengths=l[lo:hi]) for i, l in refs]
+    return bb.sentence_bleu(c, rs, bb.BleuConfig(smoothing=_POOL_DATA["smoothing"])).scores
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation on this host's
+    cores (process pool over row shards of the reference's sentence_bleu)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    b, l, v, r, smoothing = WORKLOADS[args.workload]
+    cand, refs = generate_batch(b, l, v, r)
+    bb = _ref_pkg()
+    cores = len(os.sched_getaffinity(0))
+    line = {"metric": METRIC, "unit": "sentences/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generate_batch, seed 42)",
+            "config": {"workload": f"{args.workload}: B={b} L={l} V={v} R={r} smoothing={smoothing}"}}
+    if bb is None:
+        # the oracle port, all cores via processes is not worth it for the C port: 1 thread
+        t, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=max(args.steps, 1))
+        value = b / t
+        line.update(value=value, ms_per_step=t * 1e3,
+                    cpu_baseline={"value": value, "unit": "sentences/s", "cores": 1, "kind": kind, "sample": what},
+                    e2e={"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return 0
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    workers = cores
+    per = -(-b // workers)
+    spans = [(lo, min(lo + per, b)) for lo in range(0, b, per)]
+    ctx = mp.get_context("fork")
+    with ProcessPoolExecutor(max_workers=workers, mp_context=ctx, initializer=_pool_init,
+                             initargs=(cand, refs, smoothing)) as pool:
+        for _ in range(max(args.warmup, 1)):
+            list(pool.map(_pool_work, spans))
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            list(pool.map(_pool_work, spans))
+            times.append(time.perf_counter() - t0)
+    t_pool = float(np.mean(times))
+    # threads=1 shipped configuration, for the record
+    t1, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=2)
+    value = b / t_pool
+    line.update(value=value, ms_per_step=t_pool * 1e3,
+                cpu_baseline={"value": value, "unit": "sentences/s", "cores": workers, "kind": "reference",
+                              "sample": f"batchbleu.sentence_bleu over {len(spans)} row shards in a "
+                                        f"{workers}-process pool (harness wrapper), full {b}x{l} batch per step",
+                              "single_core_value": b / t1},
+                e2e={"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_05485_b200 as tb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    b, l, v, r, smoothing = WORKLOADS[args.workload]
+    cand_np, refs_np = generate_batch(b, l, v, r, seed=42 + rank)
+    cfg = tb.BleuConfig(smoothing=smoothing)
+
+    # device-resident inputs (int32 IDs)
+    to_dev = lambda a, dt: torch.as_tensor(a).to(dev, dtype=dt)  # noqa: E731
+    cand = tb.TokenBatch(ids=to_dev(cand_np[0], torch.int32), lengths=to_dev(cand_np[1], torch.int64))
+    refs = [tb.TokenBatch(ids=to_dev(i, torch.int32), lengths=to_dev(ln, torch.int64)) for i, ln in refs_np]
+    plan = tb.SentenceBleuPlan(cand, refs, cfg)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # correctness gate before timing (bench.py:104-113 analogue): counts vs oracle on a slice
+    import oracle
+    if rank == 0:
+        st = tb.compute_stats(tb.TokenBatch(ids=cand_np[0][:32], lengths=cand_np[1][:32]),
+                              [tb.TokenBatch(ids=i[:32], lengths=ln[:32]) for i, ln in refs_np], cfg)
+        o = oracle.stats(cand_np[0][:32], cand_np[1][:32], [(i[:32], ln[:32]) for i, ln in refs_np])
+        if not np.array_equal(st.numerators, o["numerators"]):
+            print(json.dumps({"error": "equivalence check failed"}), flush=True)
+            return 2
+
+    # ---- device-resident timing: K steps of the graph-captured plan
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        plan.run()
+    plan.capture()
+    for _ in range(args.warmup):
+        plan.replay()
+    torch.cuda.synchronize(dev)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index if world == 1 else local) as clk:
+        # keep the GPU under the same load for ~1 s so that nvidia-smi (>= 50 ms
+        # period) sees the clocks of this workload; the timed steps follow directly
+        t_end = time.perf_counter() + args.clock_window
+        while time.perf_counter() < t_end:
+            for _ in range(50):
+                flush.zero_()
+                plan.replay()
+            torch.cuda.synchronize(dev)
+        for k in range(args.steps):
+            flush.zero_()                       # L2 flush between timed iterations (untimed)
+            starts[k].record(stream)
+            plan.replay()
+            ends[k].record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_local = float(np.sum(step_ms)) / 1e3
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    value = b * world * args.steps / t_max
+
+    # ---- eager public API (no graph), same device-resident inputs
+    for _ in range(2):
+        tb.sentence_bleu(cand, refs, cfg)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eager = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0.record(stream)
+        tb.sentence_bleu(cand, refs, cfg)
+        e1.record(stream)
+        e1.synchronize()
+        eager.append(e0.elapsed_time(e1))
+
+    # ---- e2e: public API with pinned HOST buffers; H2D + kernel + D2H in the timed region
+    hcand = tb.TokenBatch(ids=torch.from_numpy(cand_np[0]).pin_memory(), lengths=torch.from_numpy(cand_np[1]))
+    hrefs = [tb.TokenBatch(ids=torch.from_numpy(i).pin_memory(), lengths=torch.from_numpy(ln)) for i, ln in refs_np]
+    h2d = cand_np[0].nbytes + cand_np[1].nbytes + sum(i.nbytes + ln.nbytes for i, ln in refs_np)
+    d2h = 8 + b * (2 + cfg.max_order) * 8
+    for _ in range(2):
+        tb.sentence_bleu(hcand, hrefs, cfg)
+    barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        res = tb.sentence_bleu(hcand, hrefs, cfg)   # returns numpy: synchronous end to end
+        e2e_times.append(time.perf_counter() - t0)
+    te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = b * world * args.steps / float(te.item())
+    assert res.scores.shape == (b,)
+
+    # ---- roofline of the fused kernel (the only kernel of a step)
+    a_bytes = algorithmic_bytes([cand_np[1]] + [ln for _, ln in refs_np], v, b)
+    kernel_s = t_local / args.steps
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+        peak, peak_src = float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    achieved = a_bytes / kernel_s / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            prof = json.load(fh).get(args.workload, {})
+            traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    input_bytes = int(sum(4 * int(x.sum()) for x in [cand_np[1]] + [ln for _, ln in refs_np]))
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            t_cpu, kind, what = cpu_reference_single(cand_np, refs_np, smoothing, repeats=3)
+            cpu = {"value": b / t_cpu, "unit": "sentences/s", "cores": 1, "kind": kind,
+                   "sample": f"{what}; the full {b}x{l} batch, best of 3 after 1 warm-up"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (reference generate_batch: uniform IDs, lengths U[L/2, L], seed 42+rank)",
+            "config": {"workload": f"{args.workload}: per-sentence BLEU-4, B={b} L={l} V={v} R={r} "
+                                   f"smoothing={smoothing}, per GPU (weak scaling)",
+                       "global_batch": b * world, "seq_len": l, "parallelism": f"dp{world} (row shards)",
+                       "timed_path": "SentenceBleuPlan CUDA-graph replay of tb_bleu_stats (1 kernel/step)",
+                       "l2": "flushed (256 MiB write) before every timed step"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": a_bytes,
+                         "note": "A = SURVEY §8(d) paper-dataflow bytes; the fused kernel only reads the "
+                                 f"{input_bytes} B of int32 tokens, so frac > 1 means it beats the paper dataflow"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "sentences/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "path": "sentence_bleu(TokenBatch(pinned int64 host tensors)) -> numpy"},
+            "eager_api": {"value": b * world / (np.mean(eager) / 1e3), "unit": "sentences/s",
+                          "ms_per_step": float(np.mean(eager)),
+                          "path": "sentence_bleu(TokenBatch(CUDA tensors)) eager, per-call allocation"},
+            "gpu_launches": args.steps * plan.kernels_per_run,
+            "clocks": clk.summary(),
+            "kernel_ms": {"mean": float(np.mean(step_ms)), "min": float(np.min(step_ms)),
+                          "max": float(np.max(step_ms))},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--clock-window", type=float, default=1.5,
+                   help="seconds of sustained load sampled by nvidia-smi before the timed steps")
+    args = p.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

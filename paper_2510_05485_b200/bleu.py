@@ -1,0 +1,387 @@
+"""Per-sentence and corpus BLEU on the B200.
+
+Mirror of ``batchbleu.bleu`` (pkg/src/batchbleu/bleu.py): same public names,
+signatures, defaults, error types and result types.  The counting engine and
+the epilogue run in the fused CUDA kernel behind ``tb_bleu_stats``
+(include/tensorbleu.h); this module only validates arguments, moves host
+arrays to the device, launches, and unpacks results.
+
+Result types follow the inputs: host inputs (numpy / lists / CPU tensors)
+give numpy arrays and Python floats exactly like the reference; CUDA-tensor
+inputs give CUDA tensors and never synchronise the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+from dataclasses import dataclass
+from typing import Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _native
+from .batch import TokenBatch
+
+SMOOTHING_METHODS = ("none", "floor", "add-k", "exp")
+
+
+@dataclass(frozen=True)
+class BleuConfig:
+    """Max n-gram order, per-order weights, and smoothing (bleu.py:24-56)."""
+
+    max_order: int = 4
+    weights: Optional[Sequence[float]] = None
+    smoothing: str = "none"
+    eps: float = 0.1      # floor smoothing
+    k: float = 1.0        # add-k smoothing, orders >= 2
+
+    def __post_init__(self):
+        if self.max_order < 1:
+            raise ValueError("max_order must be >= 1")
+        if self.smoothing not in SMOOTHING_METHODS:
+            raise ValueError(
+                f"unknown smoothing {self.smoothing!r}; expected one of {SMOOTHING_METHODS}")
+        if self.eps <= 0:
+            raise ValueError("eps must be > 0")
+        if self.k <= 0:
+            raise ValueError("k must be > 0")
+        if self.weights is None:
+            w = np.full(self.max_order, 1.0 / self.max_order)
+        else:
+            w = np.asarray(self.weights, dtype=np.float64)
+            if w.shape != (self.max_order,):
+                raise ValueError(f"expected {self.max_order} weights, got shape {w.shape}")
+            if np.any(w < 0) or w.sum() <= 0:
+                raise ValueError("weights must be non-negative with positive sum")
+            w = w / w.sum()
+        object.__setattr__(self, "weights", tuple(float(x) for x in w))
+
+
+@dataclass(frozen=True)
+class SentenceStats:
+    """Per-sentence clipped numerators/denominators for orders 1..N plus
+    candidate and effective reference lengths (bleu.py:59-67).  numpy int64
+    arrays for host inputs, CUDA int64 tensors for device inputs."""
+
+    numerators: object     # (B, N) int64
+    denominators: object   # (B, N) int64
+    cand_lens: object      # (B,) int64
+    eff_ref_lens: object   # (B,) int64
+
+
+@dataclass(frozen=True)
+class BleuResult:
+    """Scores in [0, 1]; per-order precisions and BP kept for diagnostics."""
+
+    scores: Union[np.ndarray, float, torch.Tensor]
+    precisions: object
+    brevity_penalty: Union[np.ndarray, float, torch.Tensor]
+
+
+# ---------------------------------------------------------------------------
+# Scalar helpers (bleu.py:79-94) — host logic, not on the batch path.
+# ---------------------------------------------------------------------------
+def effective_ref_len(cand_len: int, ref_lens: Sequence[int]) -> int:
+    """Reference length closest to the candidate's; ties go to the shorter."""
+    if len(ref_lens) == 0:
+        raise ValueError("at least one reference length is required")
+    return min(ref_lens, key=lambda r: (abs(r - cand_len), r))
+
+
+def brevity_penalty(cand_len: int, eff_ref_len: int) -> float:
+    """exp(1 - r/c) for short candidates, 1.0 otherwise; empty candidate -> 0."""
+    if cand_len < 0:
+        raise ValueError("candidate length must be >= 0")
+    if cand_len == 0:
+        return 0.0
+    if cand_len > eff_ref_len:
+        return 1.0
+    return math.exp(1.0 - eff_ref_len / cand_len)
+
+
+def _check_batches(candidates: TokenBatch, references: Sequence[TokenBatch]) -> None:
+    """bleu.py:97-105."""
+    if not references:
+        raise ValueError("at least one reference batch is required")
+    for ref in references:
+        if ref.batch_size != candidates.batch_size:
+            raise ValueError(
+                f"reference batch size {ref.batch_size} does not match "
+                f"candidate batch size {candidates.batch_size}")
+    if len(references) > _native.TB_MAX_REFS:
+        raise ValueError(f"at most {_native.TB_MAX_REFS} reference sets are supported, "
+                         f"got {len(references)}")
+
+
+# ---------------------------------------------------------------------------
+# Host <-> device plumbing.
+# ---------------------------------------------------------------------------
+_weights_cache: dict = {}
+
+
+def _weights_arg(config: BleuConfig):
+    w = _weights_cache.get(config.weights)
+    if w is None:
+        w = (ctypes.c_double * len(config.weights))(*config.weights)
+        _weights_cache[config.weights] = w
+    return w
+
+
+class _Pinned(threading.local):
+    buf: Optional[torch.Tensor] = None
+
+
+_pinned = _Pinned()
+
+
+def _pinned_buffer(nbytes: int) -> torch.Tensor:
+    buf = _pinned.buf
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True)
+        _pinned.buf = buf
+    return buf
+
+
+def _to_device(batch: TokenBatch, device: torch.device, want64: bool):
+    """(ids, lengths, ld) on `device`; host data is copied (H2D) every call."""
+    ids, lengths = batch.ids, batch.lengths
+    if isinstance(ids, np.ndarray):
+        ids = torch.from_numpy(ids)
+        lengths = torch.from_numpy(lengths)
+    if not ids.is_cuda:
+        nb = ids.is_pinned()
+        ids = ids.to(device, non_blocking=nb)
+        lengths = lengths.to(device, non_blocking=nb)
+    elif ids.device != device:
+        raise ValueError(f"all batches must live on one device ({ids.device} vs {device})")
+    if want64 and ids.dtype != torch.int64:
+        ids = ids.to(torch.int64)
+    ld = ids.stride(0) if ids.shape[0] > 1 else ids.shape[1]
+    return ids, lengths, ld
+
+
+def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: BleuConfig,
+            mode: str):
+    """Run tb_bleu_stats.  mode: 'stats' | 'sentence' | 'corpus'.
+
+    Returns (host_mode, tensors dict on device, device-side output buffer)."""
+    _check_batches(candidates, references)
+    if config.max_order > _native.TB_MAX_ORDER:
+        raise ValueError(f"max_order > {_native.TB_MAX_ORDER} is not supported by the device path")
+    lib = _native.load()
+    host_mode = not candidates.is_device
+    device = (candidates.ids.device if not host_mode else _native.require_cuda())
+    _native.require_cuda(device)
+    batches = [candidates, *references]
+    want64 = any((b.ids.dtype != torch.int32) if isinstance(b.ids, torch.Tensor)
+                 else True for b in batches)
+    with torch.cuda.device(device):
+        dev = [_to_device(b, device, want64) for b in batches]
+        token_bytes = 8 if want64 else 4
+        B = candidates.batch_size
+        N = config.max_order
+        R = len(references)
+
+        # one output buffer: [err i32 (8 B) | payload]
+        if mode == "sentence":
+            sizes = [("scores", B, torch.float64), ("bp", B, torch.float64),
+                     ("precisions", B * N, torch.float64)]
+        elif mode == "stats":
+            sizes = [("num", B * N, torch.int64), ("den", B * N, torch.int64),
+                     ("cand_len", B, torch.int64), ("eff_ref", B, torch.int64)]
+        else:
+            sizes = [("corpus", N + 2, torch.float64), ("totals", 2 * N + 2, torch.int64)]
+        total = 8 + 8 * sum(n for _, n, _ in sizes)
+        out = torch.empty(total, dtype=torch.uint8, device=device)
+        views = {}
+        off = 8
+        for name, n, dt in sizes:
+            views[name] = out[off: off + 8 * n].view(dt)
+            off += 8 * n
+        err = out[:4].view(torch.int32)
+
+        ref_widths = np.array([b.max_len for b in references], dtype=np.int64)
+        ws_bytes = lib.tb_bleu_workspace_bytes(B, R, candidates.max_len,
+                                               ref_widths.ctypes.data, token_bytes, N)
+        if ws_bytes == 0:
+            raise ValueError("unsupported shape for the device path")
+        ws = _native.workspace.get(device, ws_bytes)
+
+        ref_ids = (ctypes.c_void_p * R)(*[d[0].data_ptr() for d in dev[1:]])
+        ref_lens = (ctypes.c_void_p * R)(*[d[1].data_ptr() for d in dev[1:]])
+        ref_ld = (ctypes.c_int64 * R)(*[d[2] for d in dev[1:]])
+        ref_w = (ctypes.c_int64 * R)(*[int(w) for w in ref_widths])
+        P = lambda name: views[name].data_ptr() if name in views else None  # noqa: E731
+        cand_ids, cand_len, cand_ld = dev[0]
+        rc = lib.tb_bleu_stats(
+            token_bytes, cand_ids.data_ptr(), cand_ld, candidates.max_len, cand_len.data_ptr(),
+            R, ref_ids, ref_ld, ref_w, ref_lens, B, N,
+            _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k,
+            _weights_arg(config),
+            P("num"), P("den"), P("cand_len"), P("eff_ref"),
+            P("scores"), P("precisions"), P("bp"),
+            P("totals"), P("corpus"),
+            err.data_ptr(), ws.data_ptr(), ws.numel(), _native.stream_handle(device))
+        _native.check(rc, "tb_bleu_stats")
+        # keep H2D sources alive until the stream is done with them
+        keep = dev
+
+    if not host_mode:
+        return False, views, None
+    # single D2H copy of [err | payload] into pinned memory, then one sync
+    pinned = _pinned_buffer(total)
+    with torch.cuda.device(device):
+        pinned[:total].copy_(out, non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()
+    del keep
+    host = pinned[:total].numpy()
+    flags = int(host[:4].view(np.int32)[0])
+    if flags:
+        _native.raise_flags(flags)
+    res = {}
+    off = 8
+    for name, n, dt in sizes:
+        npdt = np.float64 if dt == torch.float64 else np.int64
+        res[name] = host[off: off + 8 * n].view(npdt).copy()
+        off += 8 * n
+    return True, res, None
+
+
+def compute_stats(candidates: TokenBatch, references: Sequence[TokenBatch],
+                  config: BleuConfig, *, threads: int = 1,
+                  chunk_size: Optional[int] = None) -> SentenceStats:
+    """Counting pipeline for every order, reduced to per-sentence numerators
+    and denominators (bleu.py:173-210).
+
+    ``threads`` and ``chunk_size`` are accepted for signature compatibility;
+    the device path never chunks, and results never depend on them (as in the
+    reference, test_bleu.py:237-246)."""
+    host, r, _ = _launch(candidates, references, config, "stats")
+    B, N = candidates.batch_size, config.max_order
+    return SentenceStats(numerators=r["num"].reshape(B, N), denominators=r["den"].reshape(B, N),
+                         cand_lens=r["cand_len"], eff_ref_lens=r["eff_ref"])
+
+
+def sentence_bleu(candidates: TokenBatch, references: Sequence[TokenBatch],
+                  config: Optional[BleuConfig] = None, *, threads: int = 1,
+                  chunk_size: Optional[int] = None) -> BleuResult:
+    """One BLEU score per sentence of the batch (bleu.py:264-271)."""
+    config = config or BleuConfig()
+    host, r, _ = _launch(candidates, references, config, "sentence")
+    B, N = candidates.batch_size, config.max_order
+    return BleuResult(scores=r["scores"], precisions=r["precisions"].reshape(B, N),
+                      brevity_penalty=r["bp"])
+
+
+def corpus_bleu(candidates: TokenBatch, references: Sequence[TokenBatch],
+                config: Optional[BleuConfig] = None, *, threads: int = 1,
+                chunk_size: Optional[int] = None) -> BleuResult:
+    """One score for the whole batch: statistics are aggregated over
+    sentences before precisions, BP and the geometric mean (bleu.py:282-290)."""
+    config = config or BleuConfig()
+    host, r, _ = _launch(candidates, references, config, "corpus")
+    c = r["corpus"]
+    if host:
+        return BleuResult(scores=float(c[0]), precisions=c[2:].copy(),
+                          brevity_penalty=float(c[1]))
+    return BleuResult(scores=c[0], precisions=c[2:], brevity_penalty=c[1])
+
+
+def corpus_totals(candidates: TokenBatch, references: Sequence[TokenBatch],
+                  config: Optional[BleuConfig] = None) -> object:
+    """The int64 vector [Σnum_1..N | Σden_1..N | Σc | Σr] that
+    ``score_corpus_from_stats`` reduces to (bleu.py:295-300); the quantity
+    all-reduced across GPUs in sharded corpus mode."""
+    config = config or BleuConfig()
+    _, r, _ = _launch(candidates, references, config, "corpus")
+    return r["totals"]
+
+
+# ---------------------------------------------------------------------------
+# Epilogue over given statistics.
+# ---------------------------------------------------------------------------
+def _stats_on_device(stats: SentenceStats):
+    arrs = [stats.numerators, stats.denominators, stats.cand_lens, stats.eff_ref_lens]
+    if all(isinstance(a, torch.Tensor) and a.is_cuda for a in arrs):
+        dev = arrs[0].device
+        return False, dev, [a.to(torch.int64).contiguous() for a in arrs]
+    dev = _native.require_cuda()
+    out = []
+    for a in arrs:
+        a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+        out.append(torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).to(dev))
+    return True, dev, out
+
+
+def _epilogue(stats: SentenceStats, config: BleuConfig, want_scores: bool):
+    lib = _native.load()
+    host, dev, (num, den, cl, er) = _stats_on_device(stats)
+    if num.dim() != 2 or num.shape[1] != config.max_order:
+        raise ValueError(f"numerators must be (B, {config.max_order})")
+    B, N = num.shape
+    with torch.cuda.device(dev):
+        prec = torch.empty((B, N), dtype=torch.float64, device=dev)
+        bp = torch.empty(B, dtype=torch.float64, device=dev)
+        sc = torch.empty(B, dtype=torch.float64, device=dev) if want_scores else None
+        rc = lib.tb_bleu_scores(num.data_ptr(), den.data_ptr(), cl.data_ptr(), er.data_ptr(), B, N,
+                                _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k,
+                                _weights_arg(config),
+                                sc.data_ptr() if sc is not None else None, prec.data_ptr(),
+                                bp.data_ptr(), _native.stream_handle(dev))
+        _native.check(rc, "tb_bleu_scores")
+    if host:
+        return (sc.cpu().numpy() if sc is not None else None), prec.cpu().numpy(), bp.cpu().numpy()
+    return sc, prec, bp
+
+
+def apply_smoothing(stats: SentenceStats, config: BleuConfig):
+    """Per-sentence per-order precisions, shape (B, N) float64 (bleu.py:213-239)."""
+    return _epilogue(stats, config, want_scores=False)[1]
+
+
+def score_sentences_from_stats(stats: SentenceStats, config: BleuConfig) -> BleuResult:
+    """bleu.py:274-279."""
+    sc, prec, bp = _epilogue(stats, config, want_scores=True)
+    return BleuResult(scores=sc, precisions=prec, brevity_penalty=bp)
+
+
+def _totals_of(stats: SentenceStats):
+    lib = _native.load()
+    host, dev, (num, den, cl, er) = _stats_on_device(stats)
+    B, N = num.shape
+    with torch.cuda.device(dev):
+        tot = torch.empty(2 * N + 2, dtype=torch.int64, device=dev)
+        rc = lib.tb_bleu_totals(num.data_ptr(), den.data_ptr(), cl.data_ptr(), er.data_ptr(), B, N,
+                                tot.data_ptr(), _native.stream_handle(dev))
+        _native.check(rc, "tb_bleu_totals")
+    return host, tot
+
+
+def score_corpus_from_totals(totals, config: BleuConfig, host: Optional[bool] = None) -> BleuResult:
+    """Corpus epilogue on an int64 [Σnum | Σden | Σc | Σr] vector
+    (bleu.py:301-305); also the last step of sharded corpus mode."""
+    N = config.max_order
+    if isinstance(totals, torch.Tensor) and totals.is_cuda:
+        t = totals.to(torch.int64)
+        host = False if host is None else host
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(
+            totals.cpu().numpy() if isinstance(totals, torch.Tensor) else totals,
+            dtype=np.int64)).to(_native.require_cuda())
+        host = True if host is None else host
+    agg = SentenceStats(numerators=t[None, :N], denominators=t[None, N:2 * N],
+                        cand_lens=t[2 * N:2 * N + 1], eff_ref_lens=t[2 * N + 1:2 * N + 2])
+    sc, prec, bp = _epilogue(agg, config, want_scores=True)
+    if host:
+        return BleuResult(scores=float(sc[0]), precisions=prec[0].cpu().numpy(),
+                          brevity_penalty=float(bp[0]))
+    return BleuResult(scores=sc[0], precisions=prec[0], brevity_penalty=bp[0])
+
+
+def score_corpus_from_stats(stats: SentenceStats, config: BleuConfig) -> BleuResult:
+    """bleu.py:293-305."""
+    host, tot = _totals_of(stats)
+    return score_corpus_from_totals(tot, config, host=host)

@@ -1,0 +1,1350 @@
+// tensorbleu.cu — B200 (sm_100a) kernels + C ABI for the TensorBLEU hot path.
+//
+// See include/tensorbleu.h for the contract of every exported symbol and
+// DESIGN.md for the data layout and the roofline of each kernel.
+//
+// Reference behaviour followed (paths relative to /root/reference):
+//   counting   pkg/src/batchbleu/bleu.py:117-159   (_chunk_stats)
+//              pkg/src/batchbleu/ngrams.py:144-205 (packed_order_ids, segmented_bincount,
+//                                                   clipped_row_sums)
+//              pkg/src/batchbleu/_kernels.pyx:84-180 (segment_bincount, clipped_numerators)
+//   eff. ref   pkg/src/batchbleu/bleu.py:108-114
+//   epilogue   pkg/src/batchbleu/bleu.py:213-261, 274-305
+//
+// Design (one sentence group = candidate i + its R references):
+//   * one CTA owns a group at a time (grid-stride over groups, all CTAs resident);
+//   * the group's valid tokens are staged in shared memory with bulk-async copies
+//     (cp.async.bulk -> UBLKCP, completion on an mbarrier) while the CTA clears its
+//     hash table;
+//   * per order n, reference n-grams are inserted into an open-addressing table
+//     keyed by their smem position; equality is an exact token compare, so the
+//     dictionary is collision-free whatever the vocabulary or key width;
+//   * counts live in one 32-bit word per slot: high half = max-over-references
+//     count, low half = running count.  Warp-aggregated (match.any) shared
+//     atomics make hot keys (Zipf, vocab = 1) cost one atomic per warp;
+//   * the candidate pass adds to the low half; the returned old word gives both
+//     the running candidate count and the reference maximum, so min-clipping is
+//     fused into the same atomic (Σ min(cand, refmax) without a second sweep);
+//   * thread 0 finishes the group: effective reference length, smoothing, BP,
+//     weighted geometric mean, in fp64 with numpy's operation order.
+//   * corpus mode accumulates the int64 totals per CTA and the last CTA to
+//     finish runs the corpus epilogue (one launch in total).
+// Rows too wide for shared memory run the same code with the table and tokens
+// in global memory (64-bit count words).
+
+#include "../../include/tensorbleu.h"
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#define TB_VERSION_STRING "tensorbleu-b200 0.1.0 (sm_100a)"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kAccCopies = 32;         // replicated corpus accumulators (spread L2 atomics)
+constexpr int kGlobalKeyShift = 26;    // global-mode key = (ref << 26) | position
+constexpr uint32_t kFull = 0xffffffffu;
+
+thread_local char g_last_cuda_error[256] = "";
+
+int cuda_fail(cudaError_t e) {
+  snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "%s: %s", cudaGetErrorName(e),
+           cudaGetErrorString(e));
+  return TB_ERR_CUDA;
+}
+
+#define TB_CUDA(expr)                        \
+  do {                                       \
+    cudaError_t _e = (expr);                 \
+    if (_e != cudaSuccess) return cuda_fail(_e); \
+  } while (0)
+
+// --------------------------------------------------------------------------
+// Kernel parameters (passed by value as __grid_constant__).
+// --------------------------------------------------------------------------
+struct RefDesc {
+  const void* ids;
+  int64_t ld;
+  int64_t width;
+  const int64_t* len;
+};
+
+struct StatsParams {
+  const void* cand_ids;
+  int64_t cand_ld;
+  int64_t cand_width;
+  const int64_t* cand_len;
+  RefDesc refs[TB_MAX_REFS];
+  int num_refs;
+  int max_order;
+  int64_t batch;
+  // epilogue
+  int smoothing;
+  double eps;
+  double k;
+  double weights[TB_MAX_ORDER];
+  // outputs
+  int64_t* num;
+  int64_t* den;
+  int64_t* cand_len_out;
+  int64_t* eff_ref;
+  double* scores;
+  double* precisions;
+  double* bp;
+  int64_t* totals;
+  double* corpus;
+  unsigned long long* acc;  // kAccCopies x (2N+2), zero on entry and on exit
+  unsigned int* done;       // CTA completion counter, zero on entry and on exit
+  int* ws_flag;             // OR of CTA flags, zero on entry and on exit
+  int32_t* err;             // written by the last CTA
+  // hash table
+  int cap_log2;
+  // shared-memory layout (elements of the token type)
+  int cand_pad;
+  int ref_off[TB_MAX_REFS + 1];
+  // pruned shared-memory kernel: byte offsets of the per-position / table arrays
+  int off_id1, off_idn, off_live, off_ent, off_mref;
+  // global-memory mode
+  unsigned char* gtab;
+  size_t gtab_stride;
+};
+
+template <bool kSmem>
+struct Word;
+template <>
+struct Word<false> {
+  using T = unsigned long long;
+  static constexpr int kShift = 32;
+};
+
+// --------------------------------------------------------------------------
+// PTX helpers: mbarrier + bulk async copy (TMA engine, 1-D form).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// --------------------------------------------------------------------------
+// n-gram hashing / comparison.
+// --------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ uint32_t ngram_hash(const T* tok, int n) {
+  uint64_t h = 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(n);
+  for (int i = 0; i < n; ++i) {
+    h ^= static_cast<uint64_t>(tok[i]);
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  h *= 0x94D049BB133111EBull;
+  h ^= h >> 29;
+  return static_cast<uint32_t>(h);
+}
+
+template <typename T>
+__device__ __forceinline__ bool ngram_equal(const T* a, const T* b, int n) {
+  for (int i = 0; i < n; ++i)
+    if (a[i] != b[i]) return false;
+  return true;
+}
+
+// Key -> pointer to the first token of the reference n-gram it names.
+template <typename T, bool kSmem>
+struct RefTokens {
+  const T* base;                 // smem: concatenated reference rows
+  const T* const* rows;          // global: per-reference row pointers (smem array)
+  __device__ __forceinline__ int32_t key(int r, int64_t j, const int* ref_off) const {
+    if constexpr (kSmem)
+      return ref_off[r] + static_cast<int32_t>(j);
+    else
+      return (r << kGlobalKeyShift) | static_cast<int32_t>(j);
+  }
+  __device__ __forceinline__ const T* ptr(int32_t key) const {
+    if constexpr (kSmem)
+      return base + key;
+    else
+      return rows[key >> kGlobalKeyShift] + (key & ((1 << kGlobalKeyShift) - 1));
+  }
+};
+
+// Insert-or-find.  Keys only ever go EMPTY(-1) -> key once per order, so a
+// stale EMPTY read is repaired by the CAS and a non-empty read is final.
+template <typename T, bool kSmem>
+__device__ __forceinline__ int32_t table_insert(int32_t* keys, uint32_t mask, const T* gram, int n,
+                                                int32_t my_key, const RefTokens<T, kSmem>& rt) {
+  uint32_t s = ngram_hash(gram, n) & mask;
+  while (true) {
+    int32_t k = *reinterpret_cast<volatile int32_t*>(&keys[s]);
+    if (k < 0) {
+      k = atomicCAS(&keys[s], -1, my_key);
+      if (k < 0) return static_cast<int32_t>(s);
+    }
+    if (ngram_equal(rt.ptr(k), gram, n)) return static_cast<int32_t>(s);
+    s = (s + 1) & mask;
+  }
+}
+
+template <typename T, bool kSmem>
+__device__ __forceinline__ int32_t table_find(const int32_t* keys, uint32_t mask, const T* gram,
+                                              int n, const RefTokens<T, kSmem>& rt) {
+  uint32_t s = ngram_hash(gram, n) & mask;
+  while (true) {
+    const int32_t k = keys[s];
+    if (k < 0) return -1;
+    if (ngram_equal(rt.ptr(k), gram, n)) return static_cast<int32_t>(s);
+    s = (s + 1) & mask;
+  }
+}
+
+// --------------------------------------------------------------------------
+// fp64 epilogue with numpy's operation order (bleu.py:213-261).
+// __d*_rn intrinsics keep nvcc from contracting into FMAs that numpy does
+// not perform.
+// --------------------------------------------------------------------------
+__device__ void bleu_epilogue(const int64_t* num, const int64_t* den, int64_t c, int64_t r, int N,
+                              int smoothing, double eps, double kk, const double* w,
+                              double* prec_out, double* bp_out, double* score_out) {
+  double p[TB_MAX_ORDER];
+  double counter = 1.0;
+  for (int n = 0; n < N; ++n) {
+    const double nd = static_cast<double>(num[n]);
+    const double dd = static_cast<double>(den[n]);
+    const bool has_den = den[n] > 0;
+    double pn = has_den ? __ddiv_rn(nd, dd) : 0.0;            // bleu.py:222
+    const bool zero_num = (num[n] == 0) && has_den;           // bleu.py:223
+    if (smoothing == TB_SMOOTH_FLOOR) {
+      if (zero_num) pn = __ddiv_rn(eps, dd);                  // bleu.py:228
+    } else if (smoothing == TB_SMOOTH_ADD_K) {
+      if (n >= 1 && has_den) pn = __ddiv_rn(__dadd_rn(nd, kk), __dadd_rn(dd, kk));  // bleu.py:230-232
+    } else if (smoothing == TB_SMOOTH_EXP) {
+      if (zero_num) {                                         // bleu.py:234-238
+        pn = __ddiv_rn(1.0, __dmul_rn(exp2(counter), dd));
+        counter = __dadd_rn(counter, 1.0);
+      }
+    }
+    p[n] = pn;
+    if (prec_out) prec_out[n] = pn;
+  }
+  // _bp_vector, bleu.py:256-261
+  const double cd = static_cast<double>(c);
+  const double rd = static_cast<double>(r);
+  double bp = (cd > rd) ? 1.0 : exp(__dsub_rn(1.0, __ddiv_rn(rd, cd > 0.0 ? cd : 1.0)));
+  if (!(cd > 0.0)) bp = 0.0;
+  // _geo_mean_scores, bleu.py:242-253 (sequential sum over active orders)
+  bool ok = true;
+  double s = 0.0;
+  for (int n = 0; n < N; ++n) {
+    if (!(w[n] > 0.0)) continue;
+    if (p[n] > 0.0)
+      s = __dadd_rn(s, __dmul_rn(log(p[n]), w[n]));
+    else
+      ok = false;
+  }
+  double score = ok ? __dmul_rn(bp, exp(s)) : 0.0;
+  score = fmin(fmax(score, 0.0), 1.0);
+  if (bp_out) *bp_out = bp;
+  if (score_out) *score_out = score;
+}
+
+// effective reference length: closest to c, ties -> shorter (bleu.py:108-114)
+__device__ __forceinline__ int64_t closest_ref_len(int64_t c, const int64_t* ref_lens, int R) {
+  int64_t best = ref_lens[0];
+  int64_t best_d = best > c ? best - c : c - best;
+  for (int r = 1; r < R; ++r) {
+    const int64_t v = ref_lens[r];
+    const int64_t d = v > c ? v - c : c - v;
+    if (d < best_d || (d == best_d && v < best)) {
+      best = v;
+      best_d = d;
+    }
+  }
+  return best;
+}
+
+// --------------------------------------------------------------------------
+// Warp-parallel epilogue (lane n owns order n; N <= 32).  Same operations and
+// order as bleu_epilogue / numpy: the log terms are summed sequentially by
+// lane 0.  All 32 lanes of the warp must call it.
+// --------------------------------------------------------------------------
+__device__ void warp_epilogue(int64_t num, int64_t den, int64_t c, int64_t r, int N, int smoothing,
+                              double eps, double kk, double w, double* prec_out, double* bp_out,
+                              double* score_out) {
+  const int lane = threadIdx.x & 31;
+  const bool act = lane < N;
+  const double nd = static_cast<double>(num);
+  const double dd = static_cast<double>(den);
+  const bool has_den = act && den > 0;
+  const bool zero_num = has_den && num == 0;
+  double pn = has_den ? __ddiv_rn(nd, dd) : 0.0;
+  if (smoothing == TB_SMOOTH_FLOOR) {
+    if (zero_num) pn = __ddiv_rn(eps, dd);
+  } else if (smoothing == TB_SMOOTH_ADD_K) {
+    if (lane >= 1 && has_den) pn = __ddiv_rn(__dadd_rn(nd, kk), __dadd_rn(dd, kk));
+  } else if (smoothing == TB_SMOOTH_EXP) {
+    const unsigned zb = __ballot_sync(kFull, zero_num);
+    const double counter = 1.0 + static_cast<double>(__popc(zb & ((1u << lane) - 1u)));
+    if (zero_num) pn = __ddiv_rn(1.0, __dmul_rn(exp2(counter), dd));
+  }
+  if (act && prec_out) prec_out[lane] = pn;
+  const double cd = static_cast<double>(c);
+  const double rd = static_cast<double>(r);
+  double bp = (cd > rd) ? 1.0 : exp(__dsub_rn(1.0, __ddiv_rn(rd, cd > 0.0 ? cd : 1.0)));
+  if (!(cd > 0.0)) bp = 0.0;
+  const bool wpos = act && w > 0.0;
+  const bool bad = __any_sync(kFull, wpos && !(pn > 0.0));
+  const double term = (wpos && pn > 0.0) ? __dmul_rn(log(pn), w) : 0.0;
+  double s = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double t = __shfl_sync(kFull, term, n);
+    if (__shfl_sync(kFull, wpos ? 1 : 0, n)) s = __dadd_rn(s, t);
+  }
+  if (lane == 0) {
+    double score = bad ? 0.0 : __dmul_rn(bp, exp(s));
+    score = fmin(fmax(score, 0.0), 1.0);
+    if (bp_out) *bp_out = bp;
+    if (score_out) *score_out = score;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Completion protocol shared by the stats kernels: CTA flags (+ corpus
+// totals) reach the last CTA to finish, which writes *err, runs the corpus
+// epilogue and leaves the workspace zeroed for the next launch.
+// --------------------------------------------------------------------------
+__device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int& s_flags, int& s_last) {
+  const int tid = threadIdx.x;
+  const int N = p.max_order;
+  const bool corpus = p.totals != nullptr || p.corpus != nullptr;
+  const int nt = 2 * N + 2;
+  if (corpus && tid < nt && s_tot[tid]) atomicAdd(&p.acc[(blockIdx.x % kAccCopies) * nt + tid], s_tot[tid]);
+  if (tid == 0 && s_flags) atomicOr(p.ws_flag, s_flags);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(p.done, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (corpus && tid < nt) {
+      unsigned long long sum = 0;
+      for (int c = 0; c < kAccCopies; ++c) sum += atomicExch(&p.acc[c * nt + tid], 0ull);
+      s_tot[tid] = sum;
+      if (p.totals) p.totals[tid] = static_cast<int64_t>(sum);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      *p.err = atomicExch(p.ws_flag, 0);
+      *p.done = 0;
+    }
+    if (p.corpus && tid < 32) {
+      const int lane = tid;
+      warp_epilogue(lane < N ? static_cast<int64_t>(s_tot[lane]) : 0,
+                    lane < N ? static_cast<int64_t>(s_tot[N + lane]) : 0, static_cast<int64_t>(s_tot[2 * N]),
+                    static_cast<int64_t>(s_tot[2 * N + 1]), N, p.smoothing, p.eps, p.k,
+                    lane < N ? p.weights[lane] : 0.0, p.corpus + 2, p.corpus + 1, p.corpus);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// The fused per-sentence-group kernel.
+// --------------------------------------------------------------------------
+template <typename T, bool kSmem>
+__global__ void __launch_bounds__(kThreads)
+    bleu_stats_kernel(const __grid_constant__ StatsParams p) {
+  using W = typename Word<kSmem>::T;
+  constexpr int kShift = Word<kSmem>::kShift;
+  constexpr W kLow = (W(1) << kShift) - 1;
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int s_hits[TB_MAX_ORDER];
+  __shared__ int64_t s_len[TB_MAX_REFS + 1];  // [0] candidate, [1 + r] reference r
+  __shared__ const T* s_rows[TB_MAX_REFS];    // global mode: reference rows of this group
+  __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
+  __shared__ int s_last;
+  __shared__ int s_flags;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int R = p.num_refs;
+  const int N = p.max_order;
+  const uint32_t cap = 1u << p.cap_log2;
+  const uint32_t mask = cap - 1;
+  const bool corpus = p.totals != nullptr || p.corpus != nullptr;
+
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  T* s_cand = reinterpret_cast<T*>(smem + 16);
+  T* s_ref = s_cand + p.cand_pad;
+  int32_t* keys;
+  W* words;
+  if constexpr (kSmem) {
+    keys = reinterpret_cast<int32_t*>(s_ref + p.ref_off[R]);
+    words = reinterpret_cast<W*>(keys + cap);
+  } else {
+    unsigned char* g = p.gtab + static_cast<size_t>(blockIdx.x) * p.gtab_stride;
+    words = reinterpret_cast<W*>(g);
+    keys = reinterpret_cast<int32_t*>(g + static_cast<size_t>(cap) * sizeof(W));
+  }
+
+  if (tid < 2 * N + 2) s_tot[tid] = 0;
+  if (tid == 0) s_flags = 0;
+  if constexpr (kSmem) {
+    if (tid == 0) mbar_init(mbar, 1);
+  }
+  __syncthreads();
+
+  uint32_t phase = 0;
+  const T* cand_g_base = static_cast<const T*>(p.cand_ids);
+
+  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    // ---- 1. lengths (validated; clamped so that nothing reads out of bounds)
+    if (tid <= R) {
+      int64_t len, width;
+      if (tid == 0) {
+        len = p.cand_len[b];
+        width = p.cand_width;
+      } else {
+        len = p.refs[tid - 1].len[b];
+        width = p.refs[tid - 1].width;
+        if constexpr (!kSmem)
+          s_rows[tid - 1] = static_cast<const T*>(p.refs[tid - 1].ids) + b * p.refs[tid - 1].ld;
+      }
+      if (len < 0 || len > width) {
+        atomicOr(&s_flags, TB_FLAG_BAD_LENGTH);
+        len = len < 0 ? 0 : width;
+      }
+      s_len[tid] = len;
+    }
+    if (tid < N) s_hits[tid] = 0;
+    __syncthreads();
+
+    // ---- 2. stage the group's valid tokens in shared memory (bulk async copy)
+    if constexpr (kSmem) {
+      if (tid == 0) {
+        fence_proxy_async_smem();  // prior generic reads of the buffers before async writes
+        uint32_t total = 0;
+        for (int s = 0; s <= R; ++s) {
+          const T* src = s == 0 ? cand_g_base + b * p.cand_ld
+                                : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+          if ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
+            total += static_cast<uint32_t>((s_len[s] * sizeof(T)) & ~static_cast<int64_t>(15));
+        }
+        mbar_arrive_expect_tx(mbar, total);
+        for (int s = 0; s <= R; ++s) {
+          const T* src = s == 0 ? cand_g_base + b * p.cand_ld
+                                : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+          T* dst = s == 0 ? s_cand : s_ref + p.ref_off[s - 1];
+          const uint32_t bytes =
+              static_cast<uint32_t>((s_len[s] * sizeof(T)) & ~static_cast<int64_t>(15));
+          if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && bytes > 0) bulk_g2s(dst, src, bytes, mbar);
+        }
+      }
+      // tails (< 16 B) and rows whose global address is not 16-B aligned
+      for (int s = 0; s <= R; ++s) {
+        const T* src = s == 0 ? cand_g_base + b * p.cand_ld
+                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+        T* dst = s == 0 ? s_cand : s_ref + p.ref_off[s - 1];
+        const int64_t len = s_len[s];
+        const int64_t start = ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
+                                  ? static_cast<int64_t>(((len * sizeof(T)) & ~static_cast<int64_t>(15)) / sizeof(T))
+                                  : 0;
+        for (int64_t j = start + tid; j < len; j += kThreads) dst[j] = src[j];
+      }
+    }
+
+    // ---- 3. clear the table for order 1 (overlaps the bulk copy)
+    for (uint32_t s = tid; s < cap; s += kThreads) {
+      keys[s] = -1;
+      words[s] = 0;
+    }
+    if constexpr (kSmem) {
+      mbar_wait(mbar, phase);
+      phase ^= 1;
+    }
+    __syncthreads();
+
+    RefTokens<T, kSmem> rt;
+    rt.base = s_ref;
+    rt.rows = s_rows;
+    const T* cand = kSmem ? s_cand : cand_g_base + b * p.cand_ld;
+
+    // ---- 4. per order: reference counting, max-fold, clipped candidate count
+    for (int n = 1; n <= N; ++n) {
+      if (n > 1) {
+        for (uint32_t s = tid; s < cap; s += kThreads) {
+          keys[s] = -1;
+          words[s] = 0;
+        }
+        __syncthreads();
+      }
+      for (int r = 0; r < R; ++r) {
+        const int64_t cnt = s_len[1 + r] - n + 1;
+        const T* rrow = kSmem ? s_ref + p.ref_off[r] : s_rows[r];
+        // R == 1: count straight into the "max" half (no fold needed)
+        const W unit = (R == 1) ? (W(1) << kShift) : W(1);
+        for (int64_t base = 0; base < cnt; base += kThreads) {
+          const int64_t j = base + tid;
+          int32_t slot = -1;
+          if (j < cnt) slot = table_insert<T, kSmem>(keys, mask, rrow + j, n, rt.key(r, j, p.ref_off), rt);
+          const unsigned act = __ballot_sync(kFull, slot >= 0);
+          if (slot >= 0) {
+            const unsigned peers = __match_any_sync(act, slot);
+            if (lane == __ffs(peers) - 1) atomicAdd(&words[slot], unit * static_cast<W>(__popc(peers)));
+          }
+        }
+        __syncthreads();
+        if (R > 1) {  // fold: max(refmax, count_r) -> high half, reset running count
+          for (uint32_t s = tid; s < cap; s += kThreads) {
+            const W w = words[s];
+            const W c = w & kLow;
+            const W m = w >> kShift;
+            if (c) words[s] = (c > m ? c : m) << kShift;
+          }
+          __syncthreads();
+        }
+      }
+      // candidate pass: the old word carries (refmax, running count) -> clipped hit count
+      {
+        const int64_t cnt = s_len[0] - n + 1;
+        unsigned int hits = 0;
+        for (int64_t base = 0; base < cnt; base += kThreads) {
+          const int64_t j = base + tid;
+          int32_t slot = -1;
+          if (j < cnt) slot = table_find<T, kSmem>(keys, mask, cand + j, n, rt);
+          const unsigned act = __ballot_sync(kFull, slot >= 0);
+          if (slot >= 0) {
+            const unsigned peers = __match_any_sync(act, slot);
+            if (lane == __ffs(peers) - 1) {
+              const W k = static_cast<W>(__popc(peers));
+              const W old = atomicAdd(&words[slot], k);
+              const W oc = old & kLow;
+              const W m = old >> kShift;
+              const W avail = m > oc ? m - oc : 0;
+              hits += static_cast<unsigned int>(avail < k ? avail : k);
+            }
+          }
+        }
+        hits = __reduce_add_sync(kFull, hits);
+        if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+      }
+      __syncthreads();
+    }
+
+    // ---- 5. per-sentence epilogue
+    if (tid == 0) {
+      int64_t num[TB_MAX_ORDER], den[TB_MAX_ORDER];
+      const int64_t c = s_len[0];
+      for (int n = 0; n < N; ++n) {
+        num[n] = s_hits[n];
+        const int64_t d = c - n;  // max(len - (n+1) + 1, 0)
+        den[n] = d > 0 ? d : 0;
+        if (p.num) p.num[b * N + n] = num[n];
+        if (p.den) p.den[b * N + n] = den[n];
+      }
+      const int64_t r = closest_ref_len(c, &s_len[1], R);
+      if (p.cand_len_out) p.cand_len_out[b] = c;
+      if (p.eff_ref) p.eff_ref[b] = r;
+      if (p.scores || p.precisions || p.bp)
+        bleu_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, p.weights,
+                      p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
+                      p.scores ? p.scores + b : nullptr);
+      if (corpus) {
+        for (int n = 0; n < N; ++n) {
+          s_tot[n] += static_cast<unsigned long long>(num[n]);
+          s_tot[N + n] += static_cast<unsigned long long>(den[n]);
+        }
+        s_tot[2 * N] += static_cast<unsigned long long>(c);
+        s_tot[2 * N + 1] += static_cast<unsigned long long>(r);
+      }
+    }
+    __syncthreads();
+  }
+
+  finish_cta(p, s_tot, s_flags, s_last);
+}
+
+// --------------------------------------------------------------------------
+// Pruned progressive kernel (shared-memory path).
+//
+// Only n-grams that can be in the clipped intersection are ever hashed:
+//   * order 1: every candidate token is inserted (count in the entry), every
+//     reference token is looked up;
+//   * order n >= 2: a position is eligible only if its (n-1)-gram matched at
+//     order n-1 AND its last token matched at order 1 — an n-gram occurring on
+//     both sides has both properties, so skipping the rest is exact;
+//   * order-n keys are (slot of the (n-1)-prefix, slot of the last token),
+//     16 + 16 bits: one integer compare, no token re-reads (the progressive
+//     packing of ngrams.py:144-198, restricted to the live set).
+// Entry (64 bit): [key 32 | candidate count 16 | reference count 16]; a new
+// key is inserted and counted with one CAS.  The numerator is the clipped
+// intersection Σ min(cand, max_r ref) (oracle.py:36-37).
+// --------------------------------------------------------------------------
+constexpr unsigned long long kEmpty = ~0ull;
+
+__device__ __forceinline__ uint32_t fib_slot(uint32_t key, int cap_log2) {
+  return (key * 0x9E3779B1u) >> (32 - cap_log2);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t tok_hash(T t) {
+  uint64_t h = static_cast<uint64_t>(t) * 0xBF58476D1CE4E5B9ull;
+  h ^= h >> 31;
+  return static_cast<uint32_t>(h) ^ static_cast<uint32_t>(h >> 32);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 4)
+    bleu_group_kernel(const __grid_constant__ StatsParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int s_hits[TB_MAX_ORDER];
+  __shared__ int64_t s_len[TB_MAX_REFS + 1];
+  __shared__ int s_pos[TB_MAX_REFS + 1];  // position offset of row s (0 = candidate)
+  __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
+  __shared__ int s_last, s_flags, s_live;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int R = p.num_refs;
+  const int N = p.max_order;
+  const int cap_log2 = p.cap_log2;
+  const uint32_t cap = 1u << cap_log2;
+  const uint32_t mask = cap - 1;
+  const bool corpus = p.totals != nullptr || p.corpus != nullptr;
+
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  T* tok = reinterpret_cast<T*>(smem + 16);
+  uint16_t* id1 = reinterpret_cast<uint16_t*>(smem + p.off_id1);
+  uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);
+  uint8_t* live = smem + p.off_live;
+  unsigned long long* ent = reinterpret_cast<unsigned long long*>(smem + p.off_ent);
+  uint16_t* mref = reinterpret_cast<uint16_t*>(smem + p.off_mref);
+
+  if (tid < 2 * N + 2) s_tot[tid] = 0;
+  if (tid <= R) s_pos[tid] = tid == 0 ? 0 : p.cand_pad + p.ref_off[tid - 1];
+  if (tid == 0) {
+    s_flags = 0;
+    mbar_init(mbar, 1);
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  const T* cand_g = static_cast<const T*>(p.cand_ids);
+
+  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    // ---- lengths
+    if (tid <= R) {
+      int64_t len, width;
+      if (tid == 0) {
+        len = p.cand_len[b];
+        width = p.cand_width;
+      } else {
+        len = p.refs[tid - 1].len[b];
+        width = p.refs[tid - 1].width;
+      }
+      if (len < 0 || len > width) {
+        atomicOr(&s_flags, TB_FLAG_BAD_LENGTH);
+        len = len < 0 ? 0 : width;
+      }
+      s_len[tid] = len;
+    }
+    if (tid < N) s_hits[tid] = 0;
+    if (tid == 0) s_live = 0;
+    __syncthreads();
+
+    // ---- stage valid tokens (bulk async copy; tails / unaligned rows by threads)
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      uint32_t total = 0;
+      for (int s = 0; s <= R; ++s) {
+        const T* src = s == 0 ? cand_g + b * p.cand_ld
+                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
+          total += static_cast<uint32_t>((s_len[s] * sizeof(T)) & ~static_cast<int64_t>(15));
+      }
+      mbar_arrive_expect_tx(mbar, total);
+      for (int s = 0; s <= R; ++s) {
+        const T* src = s == 0 ? cand_g + b * p.cand_ld
+                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+        const uint32_t bytes = static_cast<uint32_t>((s_len[s] * sizeof(T)) & ~static_cast<int64_t>(15));
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && bytes > 0) bulk_g2s(tok + s_pos[s], src, bytes, mbar);
+      }
+    }
+    for (int s = 0; s <= R; ++s) {
+      const T* src = s == 0 ? cand_g + b * p.cand_ld
+                            : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+      const int64_t len = s_len[s];
+      const int64_t start = ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
+                                ? static_cast<int64_t>(((len * sizeof(T)) & ~static_cast<int64_t>(15)) / sizeof(T))
+                                : 0;
+      T* dst = tok + s_pos[s];
+      for (int64_t j = start + tid; j < len; j += kThreads) dst[j] = src[j];
+    }
+    for (uint32_t s = tid; s < cap; s += kThreads) {
+      ent[s] = kEmpty;
+      if (R > 1) mref[s] = 0;
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    __syncthreads();
+
+    const int clen = static_cast<int>(s_len[0]);
+    for (int n = 1; n <= N; ++n) {
+      if (n > 1) {
+        if (s_live == 0) break;  // no candidate (n-1)-gram matched: orders >= n have no hits
+        __syncthreads();         // everyone has read s_live before it is reset
+        if (tid == 0) s_live = 0;
+        for (uint32_t s = tid; s < cap; s += kThreads) {
+          ent[s] = kEmpty;
+          if (R > 1) mref[s] = 0;
+        }
+        __syncthreads();
+      }
+      // ---- (a) candidate n-grams -> table (insert + count, one CAS when new)
+      {
+        const int cnt = clen - n + 1;
+        for (int base = 0; base < cnt; base += kThreads) {
+          const int j = base + tid;
+          bool el = j < cnt;
+          uint32_t key = 0;
+          T t = 0;
+          if (el) {
+            if (n == 1) {
+              t = tok[j];
+            } else {
+              el = live[j] >= n - 1 && live[j + n - 1] >= 1;
+              key = (static_cast<uint32_t>(idn[j]) << 16) | id1[j + n - 1];
+            }
+          }
+          const unsigned act = __ballot_sync(kFull, el);
+          if (!el) continue;
+          const unsigned peers = (n == 1) ? __match_any_sync(act, t) : __match_any_sync(act, key);
+          const int leader = __ffs(peers) - 1;
+          int slot = 0;
+          if (lane == leader) {
+            const unsigned long long k16 = static_cast<unsigned long long>(__popc(peers)) << 16;
+            uint32_t s = (n == 1) ? (tok_hash(t) >> (32 - cap_log2)) : fib_slot(key, cap_log2);
+            const unsigned long long mine = (static_cast<unsigned long long>(n == 1 ? j : key) << 32) | k16;
+            while (true) {
+              unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&ent[s]);
+              if (e == kEmpty) {
+                const unsigned long long old = atomicCAS(&ent[s], kEmpty, mine);
+                if (old == kEmpty) break;
+                e = old;
+              }
+              const uint32_t ek = static_cast<uint32_t>(e >> 32);
+              if (n == 1 ? tok[ek] == t : ek == key) {
+                atomicAdd(&ent[s], k16);
+                break;
+              }
+              s = (s + 1) & mask;
+            }
+            slot = static_cast<int>(s);
+          }
+          slot = __shfl_sync(peers, slot, leader);
+          idn[j] = static_cast<uint16_t>(slot);
+          if (n == 1) id1[j] = static_cast<uint16_t>(slot);
+        }
+      }
+      __syncthreads();
+      // ---- (b) reference n-grams: look up, count, max-fold (R > 1), clip
+      unsigned int hits = 0;
+      for (int r = 0; r < R; ++r) {
+        const int off = s_pos[1 + r];
+        const int cnt = static_cast<int>(s_len[1 + r]) - n + 1;
+        for (int base = 0; base < cnt; base += kThreads) {
+          const int j = base + tid;
+          const int q = off + j;
+          bool el = j < cnt;
+          uint32_t key = 0;
+          T t = 0;
+          if (el) {
+            if (n == 1) {
+              t = tok[q];
+            } else {
+              el = live[q] >= n - 1 && live[q + n - 1] >= 1;
+              key = (static_cast<uint32_t>(idn[q]) << 16) | id1[q + n - 1];
+            }
+          }
+          const unsigned act = __ballot_sync(kFull, el);
+          if (!el) {
+            if (n == 1 && j < cnt) live[q] = 0;
+            continue;
+          }
+          const unsigned peers = (n == 1) ? __match_any_sync(act, t) : __match_any_sync(act, key);
+          const int leader = __ffs(peers) - 1;
+          int slot = -1;
+          if (lane == leader) {
+            uint32_t s = (n == 1) ? (tok_hash(t) >> (32 - cap_log2)) : fib_slot(key, cap_log2);
+            while (true) {
+              const unsigned long long e = ent[s];
+              if (e == kEmpty) break;
+              const uint32_t ek = static_cast<uint32_t>(e >> 32);
+              if (n == 1 ? tok[ek] == t : ek == key) {
+                slot = static_cast<int>(s);
+                break;
+              }
+              s = (s + 1) & mask;
+            }
+            if (slot >= 0) {
+              const unsigned k = __popc(peers);
+              const unsigned long long old = atomicAdd(&ent[slot], static_cast<unsigned long long>(k));
+              if (R == 1) {
+                const unsigned x = static_cast<unsigned>(old & 0xffff);
+                const unsigned c = static_cast<unsigned>((old >> 16) & 0xffff);
+                const unsigned avail = c > x ? c - x : 0;
+                hits += avail < k ? avail : k;
+              }
+            }
+          }
+          slot = __shfl_sync(peers, slot, leader);
+          if (slot >= 0) {
+            idn[q] = static_cast<uint16_t>(slot);
+            if (n == 1) id1[q] = static_cast<uint16_t>(slot);
+            live[q] = static_cast<uint8_t>(n);
+          } else if (n == 1) {
+            live[q] = 0;
+          }
+        }
+        if (R > 1) {
+          __syncthreads();
+          // fold reference r: m = max(m, x); numerator += min(c, m_new) - min(c, m_old)
+          for (uint32_t s = tid; s < cap; s += kThreads) {
+            const unsigned long long e = ent[s];
+            if (e == kEmpty) continue;
+            const unsigned x = static_cast<unsigned>(e & 0xffff);
+            if (!x) continue;
+            const unsigned c = static_cast<unsigned>((e >> 16) & 0xffff);
+            const unsigned m = mref[s];
+            if (x > m) {
+              hits += (c < x ? c : x) - (c < m ? c : m);
+              mref[s] = static_cast<uint16_t>(x);
+            }
+            ent[s] = e & ~0xffffull;
+          }
+        }
+        __syncthreads();
+      }
+      hits = __reduce_add_sync(kFull, hits);
+      if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+      // ---- (c) candidate liveness: does the n-gram occur in some reference?
+      {
+        const int cnt = clen - n + 1;
+        unsigned int nlive = 0;
+        for (int j = tid; j < cnt; j += kThreads) {
+          bool el = true;
+          if (n > 1) el = live[j] >= n - 1 && live[j + n - 1] >= 1;
+          bool ok = false;
+          if (el) {
+            const int s = idn[j];
+            ok = (R == 1) ? ((ent[s] & 0xffff) != 0) : (mref[s] != 0);
+          }
+          if (ok) {
+            live[j] = static_cast<uint8_t>(n);
+            ++nlive;
+          } else if (n == 1) {
+            live[j] = 0;
+          }
+        }
+        nlive = __reduce_add_sync(kFull, nlive);
+        if (lane == 0 && nlive) atomicAdd(&s_live, static_cast<int>(nlive));
+      }
+      __syncthreads();
+    }
+
+    // ---- epilogue (warp 0)
+    if (tid < 32) {
+      const int64_t c = s_len[0];
+      const int64_t num = lane < N ? static_cast<int64_t>(s_hits[lane]) : 0;
+      const int64_t den = (lane < N && c - lane > 0) ? c - lane : 0;
+      if (lane < N) {
+        if (p.num) p.num[b * N + lane] = num;
+        if (p.den) p.den[b * N + lane] = den;
+      }
+      const int64_t r = closest_ref_len(c, &s_len[1], R);
+      if (lane == 0) {
+        if (p.cand_len_out) p.cand_len_out[b] = c;
+        if (p.eff_ref) p.eff_ref[b] = r;
+      }
+      if (p.scores || p.precisions || p.bp)
+        warp_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, lane < N ? p.weights[lane] : 0.0,
+                      p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
+                      p.scores ? p.scores + b : nullptr);
+      if (corpus) {
+        if (lane < N) {
+          s_tot[lane] += static_cast<unsigned long long>(num);
+          s_tot[N + lane] += static_cast<unsigned long long>(den);
+        }
+        if (lane == 0) {
+          s_tot[2 * N] += static_cast<unsigned long long>(c);
+          s_tot[2 * N + 1] += static_cast<unsigned long long>(r);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  finish_cta(p, s_tot, s_flags, s_last);
+}
+
+// --------------------------------------------------------------------------
+// Stand-alone epilogue / totals / validation kernels.
+// --------------------------------------------------------------------------
+struct EpiParams {
+  int smoothing;
+  double eps;
+  double k;
+  double weights[TB_MAX_ORDER];
+};
+
+__global__ void bleu_scores_kernel(const int64_t* __restrict__ num, const int64_t* __restrict__ den,
+                                   const int64_t* __restrict__ cand_len,
+                                   const int64_t* __restrict__ eff_ref, int64_t batch, int N,
+                                   const __grid_constant__ EpiParams e, double* scores,
+                                   double* precisions, double* bp) {
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < batch;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    bleu_epilogue(num + b * N, den + b * N, cand_len[b], eff_ref[b], N, e.smoothing, e.eps, e.k,
+                  e.weights, precisions ? precisions + b * N : nullptr, bp ? bp + b : nullptr,
+                  scores ? scores + b : nullptr);
+  }
+}
+
+// one CTA per output column: [num_0..N-1 | den_0..N-1 | cand_len | eff_ref]
+__global__ void bleu_totals_kernel(const int64_t* __restrict__ num, const int64_t* __restrict__ den,
+                                   const int64_t* __restrict__ cand_len,
+                                   const int64_t* __restrict__ eff_ref, int64_t batch, int N,
+                                   int64_t* totals) {
+  __shared__ long long s_part[32];
+  const int col = blockIdx.x;
+  long long acc = 0;
+  for (int64_t b = threadIdx.x; b < batch; b += blockDim.x) {
+    if (col < N)
+      acc += num[b * N + col];
+    else if (col < 2 * N)
+      acc += den[b * N + (col - N)];
+    else if (col == 2 * N)
+      acc += cand_len[b];
+    else
+      acc += eff_ref[b];
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s_part[w];
+    totals[col] = t;
+  }
+}
+
+// B == 0: no flags; corpus totals zero, epilogue of zeros (bleu.py:295-305 on empty stats)
+__global__ void bleu_empty_corpus_kernel(int N, const __grid_constant__ EpiParams e, int64_t* totals,
+                                         double* corpus, int32_t* err) {
+  if (threadIdx.x != 0) return;
+  *err = 0;
+  int64_t z[TB_MAX_ORDER];
+  for (int n = 0; n < N; ++n) z[n] = 0;
+  if (totals)
+    for (int i = 0; i < 2 * N + 2; ++i) totals[i] = 0;
+  if (corpus) bleu_epilogue(z, z, 0, 0, N, e.smoothing, e.eps, e.k, e.weights, corpus + 2, corpus + 1, corpus);
+}
+
+template <typename T>
+__global__ void validate_batch_kernel(const T* __restrict__ ids, int64_t ld, int64_t width,
+                                      const int64_t* __restrict__ lengths, int64_t batch,
+                                      int32_t* err) {
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    int64_t len = lengths[b];
+    if (len < 0 || len > width) {
+      if (threadIdx.x == 0) atomicOr(err, TB_FLAG_BAD_LENGTH);
+      len = len < 0 ? 0 : width;
+    }
+    const T* row = ids + b * ld;
+    bool neg = false;
+    for (int64_t j = threadIdx.x; j < len; j += blockDim.x) neg |= row[j] < 0;
+    if (__any_sync(kFull, neg) && (threadIdx.x & 31) == 0) atomicOr(err, TB_FLAG_NEGATIVE_ID);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Device properties (cached per device).
+// --------------------------------------------------------------------------
+struct DevInfo {
+  int sms = 0;
+  int smem_optin = 0;
+  bool ok = false;
+};
+DevInfo g_dev[64];
+
+int dev_info(DevInfo** out) {
+  int dev = 0;
+  TB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return TB_ERR_UNSUPPORTED;
+  DevInfo& d = g_dev[dev];
+  if (!d.ok) {
+    TB_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    TB_CUDA(cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    d.ok = true;
+  }
+  *out = &d;
+  return TB_OK;
+}
+
+// --------------------------------------------------------------------------
+// Shape planning shared by the workspace query and the launch.
+// --------------------------------------------------------------------------
+struct Plan {
+  bool smem_mode = false;
+  int cap_log2 = 0;
+  int cand_pad = 0;
+  int ref_off[TB_MAX_REFS + 1] = {0};
+  int off_id1 = 0, off_idn = 0, off_live = 0, off_ent = 0, off_mref = 0;
+  size_t smem_bytes = 0;   // dynamic smem (smem mode)
+  size_t gtab_stride = 0;  // per-CTA table bytes (global mode)
+  int64_t grid = 0;
+  size_t acc_bytes = 0;
+  size_t ws_bytes = 0;
+};
+
+constexpr size_t kStaticSmemReserve = 2048;  // static __shared__ of the stats kernels (upper bound)
+constexpr int64_t kGlobalGridCap = 2 * 148;
+// fixed-size completion region at the start of the workspace, independent of N
+constexpr size_t kAccBytes = ((kAccCopies * (2 * TB_MAX_ORDER + 2) * 8 + 256) + 255) / 256 * 256;
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int cap_log2_for(int64_t want, int min_log2) {
+  int c = min_log2;
+  while ((int64_t(1) << c) < want) ++c;
+  return c;
+}
+
+int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_widths, int token_bytes,
+              int N, int smem_optin, int sms, Plan* pl) {
+  (void)N;
+  int64_t ref_total = 0, max_rw = 0;
+  for (int r = 0; r < R; ++r) {
+    ref_total += ref_widths[r];
+    if (ref_widths[r] > max_rw) max_rw = ref_widths[r];
+  }
+  const int64_t elems16 = 16 / token_bytes;
+  pl->acc_bytes = kAccBytes;
+
+  // ---- shared-memory (pruned progressive) layout
+  pl->cand_pad = static_cast<int>(round_up(cand_width, elems16));
+  int64_t off = 0;
+  for (int r = 0; r < R; ++r) {
+    pl->ref_off[r] = static_cast<int>(off);
+    off += round_up(ref_widths[r], elems16);
+  }
+  pl->ref_off[R] = static_cast<int>(off);
+  const int64_t ptot = pl->cand_pad + off;  // positions (candidate + references, padded)
+  const int sm_log2 = cap_log2_for(2 * cand_width, 6);
+  const int64_t sm_cap = int64_t(1) << sm_log2;
+  int64_t o = 16 + ptot * token_bytes;
+  o = round_up(o, 16);
+  const int64_t o_id1 = o;
+  o = round_up(o + ptot * 2, 16);
+  const int64_t o_idn = o;
+  o = round_up(o + ptot * 2, 16);
+  const int64_t o_live = o;
+  o = round_up(o + ptot, 16);
+  const int64_t o_ent = o;
+  o = round_up(o + sm_cap * 8, 16);
+  const int64_t o_mref = o;
+  if (R > 1) o = round_up(o + sm_cap * 2, 16);
+  const bool fits = cand_width <= 32768 && max_rw <= 65535 &&
+                    o + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin;
+  if (fits) {
+    pl->smem_mode = true;
+    pl->cap_log2 = sm_log2;
+    pl->off_id1 = static_cast<int>(o_id1);
+    pl->off_idn = static_cast<int>(o_idn);
+    pl->off_live = static_cast<int>(o_live);
+    pl->off_ent = static_cast<int>(o_ent);
+    pl->off_mref = static_cast<int>(o_mref);
+    pl->smem_bytes = static_cast<size_t>(o);
+    pl->gtab_stride = 0;
+    pl->ws_bytes = pl->acc_bytes;
+    return TB_OK;
+  }
+
+  // ---- global-memory fallback (very wide rows): position-keyed table of all reference n-grams
+  const int64_t max_w = cand_width > max_rw ? cand_width : max_rw;
+  if (max_w >= (int64_t(1) << kGlobalKeyShift)) return TB_ERR_UNSUPPORTED;
+  const int g_log2 = cap_log2_for(2 * ref_total < 32 ? 32 : 2 * ref_total, 5);
+  if (g_log2 > 30) return TB_ERR_UNSUPPORTED;
+  pl->smem_mode = false;
+  pl->cap_log2 = g_log2;
+  pl->smem_bytes = 16;
+  pl->gtab_stride = static_cast<size_t>(round_up((int64_t(1) << g_log2) * (8 + 4), 256));
+  const int64_t cap_grid = sms > 0 ? 2 * sms : kGlobalGridCap;
+  pl->grid = batch < cap_grid ? batch : cap_grid;
+  if (pl->grid < 1) pl->grid = 1;
+  pl->ws_bytes = pl->acc_bytes + static_cast<size_t>(pl->grid) * pl->gtab_stride;
+  return TB_OK;
+}
+
+template <typename K>
+int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool persistent_fill,
+                  size_t* attr_set, cudaStream_t stream) {
+  int dev = 0;
+  TB_CUDA(cudaGetDevice(&dev));
+  if (pl.smem_bytes > 48 * 1024 && attr_set[dev & 63] < pl.smem_bytes) {
+    TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(pl.smem_bytes)));
+    attr_set[dev & 63] = pl.smem_bytes;
+  }
+  int64_t grid = pl.grid;
+  if (persistent_fill) {
+    int occ = 0;
+    TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, pl.smem_bytes));
+    if (occ < 1) occ = 1;
+    const int64_t resident = static_cast<int64_t>(occ) * sms;
+    grid = prm.batch < resident ? prm.batch : resident;
+  }
+  kern<<<static_cast<unsigned>(grid), kThreads, pl.smem_bytes, stream>>>(prm);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+template <typename T>
+int launch_stats(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream) {
+  if (pl.smem_mode) {
+    static size_t attr_set[64] = {0};
+    return launch_kernel(bleu_group_kernel<T>, prm, pl, sms, true, attr_set, stream);
+  }
+  static size_t attr_set[64] = {0};
+  return launch_kernel(bleu_stats_kernel<T, false>, prm, pl, sms, false, attr_set, stream);
+}
+
+void fill_epi(EpiParams* e, int N, int smoothing, double eps, double k, const double* weights) {
+  e->smoothing = smoothing;
+  e->eps = eps;
+  e->k = k;
+  for (int n = 0; n < TB_MAX_ORDER; ++n) e->weights[n] = n < N ? weights[n] : 0.0;
+}
+
+int check_epi(int N, int smoothing, double eps, double k, const double* weights) {
+  if (N < 1) return TB_ERR_INVALID_ARG;
+  if (N > TB_MAX_ORDER) return TB_ERR_UNSUPPORTED;
+  if (smoothing < TB_SMOOTH_NONE || smoothing > TB_SMOOTH_EXP) return TB_ERR_INVALID_ARG;
+  if (!(eps > 0) || !(k > 0)) return TB_ERR_INVALID_ARG;
+  if (!weights) return TB_ERR_INVALID_ARG;
+  for (int n = 0; n < N; ++n)
+    if (!(weights[n] >= 0)) return TB_ERR_INVALID_ARG;
+  return TB_OK;
+}
+
+}  // namespace
+
+// ==========================================================================
+// Segment kernels for the plugin surface live in plugin.cu; C ABI below.
+// ==========================================================================
+extern "C" {
+
+const char* tb_version(void) { return TB_VERSION_STRING; }
+
+const char* tb_strerror(int code) {
+  switch (code) {
+    case TB_OK: return "ok";
+    case TB_ERR_INVALID_ARG: return "invalid argument";
+    case TB_ERR_CAPACITY: return "capacity exceeded (index space overflows int64)";
+    case TB_ERR_CUDA: return "CUDA error";
+    case TB_ERR_UNSUPPORTED: return "unsupported by the device path";
+    case TB_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown error";
+  }
+}
+
+const char* tb_last_cuda_error(void) { return g_last_cuda_error; }
+
+size_t tb_bleu_workspace_bytes(int64_t batch, int32_t num_refs, int64_t cand_width,
+                               const int64_t* ref_widths, int32_t token_bytes, int32_t max_order) {
+  if (num_refs < 1 || num_refs > TB_MAX_REFS || max_order < 1 || max_order > TB_MAX_ORDER) return 0;
+  if (token_bytes != 4 && token_bytes != 8) return 0;
+  DevInfo* d = nullptr;
+  int smem_optin = 227 * 1024, sms = 148;
+  if (dev_info(&d) == TB_OK) {
+    smem_optin = d->smem_optin;
+    sms = d->sms;
+  }
+  Plan pl;
+  if (make_plan(batch, num_refs, cand_width, ref_widths, token_bytes, max_order, smem_optin, sms, &pl) != TB_OK)
+    return 0;
+  return pl.ws_bytes;
+}
+
+int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int64_t cand_width,
+                  const int64_t* cand_len, int32_t num_refs, const void* const* ref_ids,
+                  const int64_t* ref_ld, const int64_t* ref_width, const int64_t* const* ref_len,
+                  int64_t batch, int32_t max_order, int32_t smoothing, double eps, double k,
+                  const double* weights, int64_t* num_out, int64_t* den_out, int64_t* cand_len_out,
+                  int64_t* eff_ref_out, double* scores_out, double* precisions_out, double* bp_out,
+                  int64_t* totals_out, double* corpus_out, int32_t* err_flag, void* workspace,
+                  size_t workspace_bytes, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (token_bytes != 4 && token_bytes != 8) return TB_ERR_INVALID_ARG;
+  if (num_refs < 1) return TB_ERR_INVALID_ARG;
+  if (num_refs > TB_MAX_REFS) return TB_ERR_UNSUPPORTED;
+  if (batch < 0 || cand_width < 0 || cand_ld < cand_width) return TB_ERR_INVALID_ARG;
+  int rc = check_epi(max_order, smoothing, eps, k, weights);
+  if (rc != TB_OK) return rc;
+  if (!ref_ids || !ref_ld || !ref_width || !ref_len || !err_flag) return TB_ERR_INVALID_ARG;
+  for (int r = 0; r < num_refs; ++r)
+    if (ref_width[r] < 0 || ref_ld[r] < ref_width[r]) return TB_ERR_INVALID_ARG;
+  if (batch == 0) {
+    EpiParams e;
+    fill_epi(&e, max_order, smoothing, eps, k, weights);
+    bleu_empty_corpus_kernel<<<1, 32, 0, stream>>>(max_order, e, totals_out, corpus_out, err_flag);
+    TB_CUDA(cudaGetLastError());
+    return TB_OK;
+  }
+  if ((!cand_ids && cand_width > 0) || !cand_len) return TB_ERR_INVALID_ARG;
+
+  DevInfo* d = nullptr;
+  rc = dev_info(&d);
+  if (rc != TB_OK) return rc;
+  Plan pl;
+  rc = make_plan(batch, num_refs, cand_width, ref_width, token_bytes, max_order, d->smem_optin, d->sms, &pl);
+  if (rc != TB_OK) return rc;
+  if (workspace_bytes < pl.ws_bytes || (pl.ws_bytes && !workspace)) return TB_ERR_WORKSPACE;
+
+  StatsParams prm;
+  memset(&prm, 0, sizeof(prm));
+  prm.cand_ids = cand_ids;
+  prm.cand_ld = cand_ld;
+  prm.cand_width = cand_width;
+  prm.cand_len = cand_len;
+  for (int r = 0; r < num_refs; ++r) {
+    prm.refs[r].ids = ref_ids[r];
+    prm.refs[r].ld = ref_ld[r];
+    prm.refs[r].width = ref_width[r];
+    prm.refs[r].len = ref_len[r];
+    if (!ref_len[r] || (!ref_ids[r] && ref_width[r] > 0)) return TB_ERR_INVALID_ARG;
+  }
+  prm.num_refs = num_refs;
+  prm.max_order = max_order;
+  prm.batch = batch;
+  prm.smoothing = smoothing;
+  prm.eps = eps;
+  prm.k = k;
+  for (int n = 0; n < TB_MAX_ORDER; ++n) prm.weights[n] = n < max_order ? weights[n] : 0.0;
+  prm.num = num_out;
+  prm.den = den_out;
+  prm.cand_len_out = cand_len_out;
+  prm.eff_ref = eff_ref_out;
+  prm.scores = scores_out;
+  prm.precisions = precisions_out;
+  prm.bp = bp_out;
+  prm.totals = totals_out;
+  prm.corpus = corpus_out;
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  prm.acc = reinterpret_cast<unsigned long long*>(ws);
+  prm.done = reinterpret_cast<unsigned int*>(ws + pl.acc_bytes - 256);
+  prm.ws_flag = reinterpret_cast<int*>(ws + pl.acc_bytes - 256 + 4);
+  prm.err = err_flag;
+  prm.cap_log2 = pl.cap_log2;
+  prm.cand_pad = pl.cand_pad;
+  for (int r = 0; r <= num_refs; ++r) prm.ref_off[r] = pl.ref_off[r];
+  prm.off_id1 = pl.off_id1;
+  prm.off_idn = pl.off_idn;
+  prm.off_live = pl.off_live;
+  prm.off_ent = pl.off_ent;
+  prm.off_mref = pl.off_mref;
+  prm.gtab = pl.smem_mode ? nullptr : ws + pl.acc_bytes;
+  prm.gtab_stride = pl.gtab_stride;
+
+  if (token_bytes == 4) return launch_stats<int32_t>(prm, pl, d->sms, stream);
+  return launch_stats<int64_t>(prm, pl, d->sms, stream);
+}
+
+int tb_bleu_scores(const int64_t* num, const int64_t* den, const int64_t* cand_len,
+                   const int64_t* eff_ref, int64_t batch, int32_t max_order, int32_t smoothing,
+                   double eps, double k, const double* weights, double* scores_out,
+                   double* precisions_out, double* bp_out, void* stream) {
+  int rc = check_epi(max_order, smoothing, eps, k, weights);
+  if (rc != TB_OK) return rc;
+  if (batch < 0) return TB_ERR_INVALID_ARG;
+  if (batch == 0) return TB_OK;
+  if (!num || !den || !cand_len || !eff_ref) return TB_ERR_INVALID_ARG;
+  EpiParams e;
+  fill_epi(&e, max_order, smoothing, eps, k, weights);
+  const int threads = 128;
+  int64_t blocks = (batch + threads - 1) / threads;
+  if (blocks > 65535) blocks = 65535;
+  bleu_scores_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      num, den, cand_len, eff_ref, batch, max_order, e, scores_out, precisions_out, bp_out);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_bleu_totals(const int64_t* num, const int64_t* den, const int64_t* cand_len,
+                   const int64_t* eff_ref, int64_t batch, int32_t max_order, int64_t* totals_out,
+                   void* stream) {
+  if (max_order < 1) return TB_ERR_INVALID_ARG;
+  if (max_order > TB_MAX_ORDER) return TB_ERR_UNSUPPORTED;
+  if (batch < 0 || !totals_out) return TB_ERR_INVALID_ARG;
+  if (batch > 0 && (!num || !den || !cand_len || !eff_ref)) return TB_ERR_INVALID_ARG;
+  bleu_totals_kernel<<<2 * max_order + 2, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      num, den, cand_len, eff_ref, batch, max_order, totals_out);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_validate_batch(int32_t token_bytes, const void* ids, int64_t ld, int64_t width,
+                      const int64_t* lengths, int64_t batch, int32_t* err_flag, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (token_bytes != 4 && token_bytes != 8) return TB_ERR_INVALID_ARG;
+  if (batch < 0 || width < 0 || ld < width || !err_flag) return TB_ERR_INVALID_ARG;
+  if (batch == 0) return TB_OK;
+  if (!lengths || (!ids && width > 0)) return TB_ERR_INVALID_ARG;
+  int64_t grid = batch < 4096 ? batch : 4096;
+  if (token_bytes == 4)
+    validate_batch_kernel<int32_t><<<static_cast<unsigned>(grid), 256, 0, stream>>>(
+        static_cast<const int32_t*>(ids), ld, width, lengths, batch, err_flag);
+  else
+    validate_batch_kernel<int64_t><<<static_cast<unsigned>(grid), 256, 0, stream>>>(
+        static_cast<const int64_t*>(ids), ld, width, lengths, batch, err_flag);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+}  // extern "C"
