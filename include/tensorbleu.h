@@ -18,9 +18,9 @@
  *  - Errors that depend only on host arguments are returned immediately as a
  *    TB_ERR_* code.  Errors that depend on device data (a length outside
  *    [0, width], a negative token ID in a valid position, a compact ID outside
- *    [0, U)) are reported in the device int32 `*err_flag` (TB_FLAG_* bits;
- *    tb_bleu_stats writes it, the other calls OR into it); the caller reads
- *    it after synchronising and raises.
+ *    [0, U)) are OR-ed into the device int32 `*err_flag` (TB_FLAG_* bits;
+ *    see tb_bleu_stats for its corpus-mode exception); the caller reads it
+ *    after synchronising and raises.
  *  - Token IDs are int32 or int64 (`token_bytes` = 4 or 8), row-major with a
  *    leading dimension `ld` (elements).  Lengths are int64, as in
  *    `TokenBatch` (pkg/src/batchbleu/batch.py:22-37).
@@ -107,8 +107,9 @@ size_t tb_bleu_workspace_bytes(int64_t batch, int32_t num_refs,
  *  bp_out            device (B,) fp64 or NULL       (BleuResult.brevity_penalty)
  *  totals_out        device (2N+2,) int64 or NULL   [sum num_n | sum den_n | sum c | sum r]
  *  corpus_out        device (N+2,) fp64 or NULL     [score, bp, precisions_n]  (corpus epilogue)
- *  err_flag          device int32, WRITTEN (0 or TB_FLAG_* bits) by the launch —
- *                    no pre-zeroing needed.
+ *  err_flag          device int32.  Per-sentence launches OR TB_FLAG_* bits into
+ *                    it (the caller zeroes it; it is sticky across launches);
+ *                    launches with totals_out/corpus_out WRITE it (0 or bits).
  * num_out/den_out may be NULL when only scores or corpus outputs are wanted.
  */
 int tb_bleu_stats(int32_t token_bytes,

@@ -202,6 +202,8 @@ def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: Bl
             views[name] = out[off: off + 8 * n].view(dt)
             off += 8 * n
         err = out[:4].view(torch.int32)
+        if host_mode or mode == "corpus":
+            err.zero_()  # per-sentence launches OR their flags into it (include/tensorbleu.h)
 
         ref_widths = np.array([b.max_len for b in references], dtype=np.int64)
         ws_bytes = lib.tb_bleu_workspace_bytes(B, R, candidates.max_len,

@@ -109,7 +109,7 @@ struct StatsParams {
   int cand_pad;
   int ref_off[TB_MAX_REFS + 1];
   // pruned shared-memory kernel: byte offsets of the per-position / table arrays
-  int off_id1, off_idn, off_live, off_ent, off_mref;
+  int off_id1, off_idn, off_live, off_ent, off_mref, off_kc, off_lists, off_seg;
   // global-memory mode
   unsigned char* gtab;
   size_t gtab_stride;
@@ -355,15 +355,23 @@ __device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int&
   const int tid = threadIdx.x;
   const int N = p.max_order;
   const bool corpus = p.totals != nullptr || p.corpus != nullptr;
+  if (!corpus) {  // no cross-CTA work: report flags directly (the caller zeroed *err)
+    __syncthreads();
+    if (tid == 0 && s_flags) atomicOr(p.err, s_flags);
+    return;
+  }
   const int nt = 2 * N + 2;
   if (corpus && tid < nt && s_tot[tid]) atomicAdd(&p.acc[(blockIdx.x % kAccCopies) * nt + tid], s_tot[tid]);
   if (tid == 0 && s_flags) atomicOr(p.ws_flag, s_flags);
-  __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(p.done, 1u) == gridDim.x - 1);
+  if (tid == 0) {
+    // release this CTA's accumulator/flag updates, acquire everyone else's
+    unsigned int prev;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.done) : "memory");
+    s_last = (prev == gridDim.x - 1);
+  }
   __syncthreads();
   if (s_last) {
-    __threadfence();
     if (corpus && tid < nt) {
       unsigned long long sum = 0;
       for (int c = 0; c < kAccCopies; ++c) sum += atomicExch(&p.acc[c * nt + tid], 0ull);
@@ -606,29 +614,126 @@ __global__ void __launch_bounds__(kThreads)
 // Pruned progressive kernel (shared-memory path).
 //
 // Only n-grams that can be in the clipped intersection are ever hashed:
-//   * order 1: every candidate token is inserted (count in the entry), every
-//     reference token is looked up;
-//   * order n >= 2: a position is eligible only if its (n-1)-gram matched at
-//     order n-1 AND its last token matched at order 1 — an n-gram occurring on
-//     both sides has both properties, so skipping the rest is exact;
+//   * order 1: every candidate token is inserted (count kept in the entry),
+//     every reference token is looked up;
+//   * order n >= 2: a position is visited only if its (n-1)-gram matched the
+//     other side at order n-1 (it is on that order's live list) and its last
+//     token matched at order 1 — an n-gram occurring on both sides has both
+//     properties, so skipping everything else is exact;
 //   * order-n keys are (slot of the (n-1)-prefix, slot of the last token),
 //     16 + 16 bits: one integer compare, no token re-reads (the progressive
 //     packing of ngrams.py:144-198, restricted to the live set).
 // Entry (64 bit): [key 32 | candidate count 16 | reference count 16]; a new
 // key is inserted and counted with one CAS.  The numerator is the clipped
-// intersection Σ min(cand, max_r ref) (oracle.py:36-37).
+// intersection sum_g min(cand_g, max_r ref_{r,g}) (oracle.py:36-37).
+// Live lists are built with warp-aggregated appends, so orders >= 2 cost
+// time proportional to the matching n-grams only.
 // --------------------------------------------------------------------------
-constexpr unsigned long long kEmpty = ~0ull;
 
-__device__ __forceinline__ uint32_t fib_slot(uint32_t key, int cap_log2) {
-  return (key * 0x9E3779B1u) >> (32 - cap_log2);
+// Debug-only phase timestamps (build with -DTB_PHASES; see tools/phase_profile.py)
+#ifdef TB_PHASES
+__device__ unsigned long long* g_tb_phases;
+#define TB_MARK(k)                                                                        \
+  do {                                                                                   \
+    if (threadIdx.x == 0 && g_tb_phases && (k) < 32) {                                   \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      g_tb_phases[blockIdx.x * 32 + (k)] = t_;                                           \
+    }                                                                                    \
+  } while (0)
+#else
+#define TB_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
+// 32-bit multiplicative hash of a token; use the TOP bits (h >> (32 - bits))
+template <typename T>
+__device__ __forceinline__ uint32_t tok_hash32(T t) {
+  if constexpr (sizeof(T) == 4) {
+    return static_cast<uint32_t>(t) * 0x9E3779B1u;
+  } else {
+    const uint64_t h = static_cast<uint64_t>(t) * 0x9E3779B97F4A7C15ull;
+    return static_cast<uint32_t>(h >> 32);
+  }
 }
 
-template <typename T>
-__device__ __forceinline__ uint32_t tok_hash(T t) {
-  uint64_t h = static_cast<uint64_t>(t) * 0xBF58476D1CE4E5B9ull;
-  h ^= h >> 31;
-  return static_cast<uint32_t>(h) ^ static_cast<uint32_t>(h >> 32);
+// warp-aggregated append of `val` to list[*count] for lanes with `pred`;
+// every lane of the warp must call it
+__device__ __forceinline__ void list_append(uint16_t* list, int* count, bool pred, int val) {
+  const unsigned m = __ballot_sync(kFull, pred);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(kFull, base, leader);
+  if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(val);
+}
+
+// Lookup of `key` (order n >= 2 packed key, or a token at order 1) in the
+// bucketed table.  A present key always sits in its home bucket unless that
+// bucket was full when it was inserted, so a lookup stops at the first bucket
+// with an empty entry.  The home slot is checked first (keys usually win their
+// home slot), which makes most lookups a single 4-byte load.
+template <typename EqF>
+__device__ __forceinline__ int table_find(const uint32_t* ent, uint32_t home, uint32_t bmask, EqF eq) {
+  const uint32_t e0 = ent[home];
+  if (e0 == ~0u) return -1;
+  if (eq(e0 >> 16)) return static_cast<int>(home);
+  uint32_t bk = home >> 2;
+  while (true) {
+    const uint4 q = reinterpret_cast<const uint4*>(ent)[bk];
+    const uint32_t e[4] = {q.x, q.y, q.z, q.w};
+    bool full = true;
+    int slot = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (e[k] == ~0u)
+        full = false;
+      else if (slot < 0 && 4 * bk + k != home && eq(e[k] >> 16))
+        slot = static_cast<int>(4 * bk + k);
+    }
+    if (slot >= 0 || !full) return slot;
+    bk = (bk + 1) & bmask;
+  }
+}
+
+// Round 2 of the candidate insert for a position that lost its home slot to a
+// different key: CAS into the first empty entry from the home bucket on, or add
+// to an equal key inserted by another loser.
+template <typename EqF>
+__device__ __forceinline__ uint32_t table_insert_loser(uint32_t* ent, uint32_t home, uint32_t bmask,
+                                                       uint32_t mine, EqF eq) {
+  uint32_t bk = home >> 2;
+  while (true) {
+    uint4 q;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                 : "r"(smem_u32(ent + 4 * bk)));
+    const uint32_t e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t v = e[k];
+      if (v == ~0u) {
+        v = atomicCAS(&ent[4 * bk + k], ~0u, mine);
+        if (v == ~0u) return 4 * bk + k;
+      }
+      if (eq(v >> 16)) {
+        atomicAdd(&ent[4 * bk + k], 1u);
+        return 4 * bk + k;
+      }
+    }
+    bk = (bk + 1) & bmask;
+  }
+}
+
+// reference-count half-words packed in u32 words (32-bit atomics only)
+__device__ __forceinline__ void xc_add(uint32_t* xcw, int s) { atomicAdd(&xcw[s >> 1], 1u << ((s & 1) * 16)); }
+__device__ __forceinline__ uint32_t xc_get(const uint32_t* xcw, int s) { return (xcw[s >> 1] >> ((s & 1) * 16)) & 0xffffu; }
+__device__ __forceinline__ uint32_t xc_take(uint32_t* xcw, int s) {
+  const uint32_t m = 0xffffu << ((s & 1) * 16);
+  return (atomicAnd(&xcw[s >> 1], ~m) & m) >> ((s & 1) * 16);
 }
 
 template <typename T>
@@ -639,7 +744,9 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int64_t s_len[TB_MAX_REFS + 1];
   __shared__ int s_pos[TB_MAX_REFS + 1];  // position offset of row s (0 = candidate)
   __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
-  __shared__ int s_last, s_flags, s_live;
+  __shared__ int s_last, s_flags;
+  __shared__ int s_nlc[2], s_nins[2];    // candidate live / inserted list lengths (by order parity)
+  __shared__ int s_nlr[2][TB_MAX_REFS];  // live reference list lengths
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -647,7 +754,6 @@ __global__ void __launch_bounds__(kThreads, 4)
   const int N = p.max_order;
   const int cap_log2 = p.cap_log2;
   const uint32_t cap = 1u << cap_log2;
-  const uint32_t mask = cap - 1;
   const bool corpus = p.totals != nullptr || p.corpus != nullptr;
 
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
@@ -655,21 +761,57 @@ __global__ void __launch_bounds__(kThreads, 4)
   uint16_t* id1 = reinterpret_cast<uint16_t*>(smem + p.off_id1);
   uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);
   uint8_t* live = smem + p.off_live;
-  unsigned long long* ent = reinterpret_cast<unsigned long long*>(smem + p.off_ent);
-  uint16_t* mref = reinterpret_cast<uint16_t*>(smem + p.off_mref);
+  uint32_t* ent = reinterpret_cast<uint32_t*>(smem + p.off_ent);   // [cand position 16 | cand count 16]
+  uint32_t* xcw = ent + cap;                                        // reference counts, 16 bit, paired
+  uint16_t* mref = reinterpret_cast<uint16_t*>(smem + p.off_mref);  // max over references (R > 1)
+  uint32_t* kc = reinterpret_cast<uint32_t*>(smem + p.off_kc);      // order-n key of candidate positions
+  uint16_t* lc = reinterpret_cast<uint16_t*>(smem + p.off_lists);   // candidate positions live at order n-1 / n
+  const int cpad = p.cand_pad;
+  const int rtot = p.ref_off[R];
+  uint16_t* lins = lc + cpad;                                       // candidate positions inserted at order n
+  uint16_t* lrbase = lc + 2 * cpad;                                 // reference lists, two parities
+  const uint32_t hshift = 32 - cap_log2;  // home slot = top bits of the hash
+  const uint32_t bmask = (cap >> 2) - 1;  // buckets of 4 slots (one 16-byte load)
+  const T* cand_g = static_cast<const T*>(p.cand_ids);
+
+  // Stage the full rows of group b (widths are known without reading lengths):
+  // bulk copies of the 16-byte-aligned body; the < 16-byte tails and rows whose
+  // global address is unaligned are copied by the threads before the barrier.
+  auto issue_stage = [&](int64_t b) {
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      uint32_t total = 0;
+      for (int s = 0; s <= R; ++s) {
+        const T* src = s == 0 ? cand_g + b * p.cand_ld
+                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+        const int64_t w = s == 0 ? p.cand_width : p.refs[s - 1].width;
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) total += static_cast<uint32_t>((w * sizeof(T)) & ~int64_t(15));
+      }
+      mbar_arrive_expect_tx(mbar, total);
+      for (int s = 0; s <= R; ++s) {
+        const T* src = s == 0 ? cand_g + b * p.cand_ld
+                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+        const int64_t w = s == 0 ? p.cand_width : p.refs[s - 1].width;
+        const uint32_t bytes = static_cast<uint32_t>((w * sizeof(T)) & ~int64_t(15));
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && bytes > 0)
+          bulk_g2s(tok + (s == 0 ? 0 : cpad + p.ref_off[s - 1]), src, bytes, mbar);
+      }
+    }
+  };
 
   if (tid < 2 * N + 2) s_tot[tid] = 0;
-  if (tid <= R) s_pos[tid] = tid == 0 ? 0 : p.cand_pad + p.ref_off[tid - 1];
+  if (tid <= R) s_pos[tid] = tid == 0 ? 0 : cpad + p.ref_off[tid - 1];
   if (tid == 0) {
     s_flags = 0;
     mbar_init(mbar, 1);
   }
+  if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
   __syncthreads();
+  TB_MARK(0);
   uint32_t phase = 0;
-  const T* cand_g = static_cast<const T*>(p.cand_ids);
 
   for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
-    // ---- lengths
+    // ---- lengths, per-group state (the token copy is already in flight)
     if (tid <= R) {
       int64_t len, width;
       if (tid == 0) {
@@ -686,207 +828,238 @@ __global__ void __launch_bounds__(kThreads, 4)
       s_len[tid] = len;
     }
     if (tid < N) s_hits[tid] = 0;
-    if (tid == 0) s_live = 0;
-    __syncthreads();
-
-    // ---- stage valid tokens (bulk async copy; tails / unaligned rows by threads)
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      uint32_t total = 0;
-      for (int s = 0; s <= R; ++s) {
-        const T* src = s == 0 ? cand_g + b * p.cand_ld
-                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
-          total += static_cast<uint32_t>((s_len[s] * sizeof(T)) & ~static_cast<int64_t>(15));
-      }
-      mbar_arrive_expect_tx(mbar, total);
-      for (int s = 0; s <= R; ++s) {
-        const T* src = s == 0 ? cand_g + b * p.cand_ld
-                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
-        const uint32_t bytes = static_cast<uint32_t>((s_len[s] * sizeof(T)) & ~static_cast<int64_t>(15));
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && bytes > 0) bulk_g2s(tok + s_pos[s], src, bytes, mbar);
-      }
+    if (tid < 2) {
+      s_nlc[tid] = 0;
+      s_nins[tid] = 0;
     }
+    if (tid < 2 * R) s_nlr[tid / R][tid % R] = 0;
+    // tails / unaligned rows
     for (int s = 0; s <= R; ++s) {
       const T* src = s == 0 ? cand_g + b * p.cand_ld
                             : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
-      const int64_t len = s_len[s];
+      const int64_t w = s == 0 ? p.cand_width : p.refs[s - 1].width;
       const int64_t start = ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
-                                ? static_cast<int64_t>(((len * sizeof(T)) & ~static_cast<int64_t>(15)) / sizeof(T))
+                                ? static_cast<int64_t>(((w * sizeof(T)) & ~int64_t(15)) / sizeof(T))
                                 : 0;
-      T* dst = tok + s_pos[s];
-      for (int64_t j = start + tid; j < len; j += kThreads) dst[j] = src[j];
+      T* dst = tok + (s == 0 ? 0 : cpad + p.ref_off[s - 1]);
+      for (int64_t j = start + tid; j < w; j += kThreads) dst[j] = src[j];
     }
-    for (uint32_t s = tid; s < cap; s += kThreads) {
-      ent[s] = kEmpty;
-      if (R > 1) mref[s] = 0;
+    // clear the table (entries EMPTY, reference counts 0); later orders clear only used slots
+    for (uint32_t s = tid; s < cap / 4; s += kThreads) reinterpret_cast<uint4*>(ent)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (uint32_t s = tid; s < cap / 8; s += kThreads) {
+      reinterpret_cast<uint4*>(xcw)[s] = make_uint4(0, 0, 0, 0);
+      if (R > 1) reinterpret_cast<uint4*>(mref)[s] = make_uint4(0, 0, 0, 0);
     }
     mbar_wait(mbar, phase);
     phase ^= 1;
     __syncthreads();
+    TB_MARK(2);
 
     const int clen = static_cast<int>(s_len[0]);
-    for (int n = 1; n <= N; ++n) {
-      if (n > 1) {
-        if (s_live == 0) break;  // no candidate (n-1)-gram matched: orders >= n have no hits
-        __syncthreads();         // everyone has read s_live before it is reset
-        if (tid == 0) s_live = 0;
-        for (uint32_t s = tid; s < cap; s += kThreads) {
-          ent[s] = kEmpty;
-          if (R > 1) mref[s] = 0;
-        }
-        __syncthreads();
-      }
-      // ---- (a) candidate n-grams -> table (insert + count, one CAS when new)
-      {
-        const int cnt = clen - n + 1;
-        for (int base = 0; base < cnt; base += kThreads) {
-          const int j = base + tid;
-          bool el = j < cnt;
-          uint32_t key = 0;
-          T t = 0;
-          if (el) {
-            if (n == 1) {
-              t = tok[j];
-            } else {
-              el = live[j] >= n - 1 && live[j + n - 1] >= 1;
-              key = (static_cast<uint32_t>(idn[j]) << 16) | id1[j + n - 1];
-            }
-          }
-          const unsigned act = __ballot_sync(kFull, el);
-          if (!el) continue;
-          const unsigned peers = (n == 1) ? __match_any_sync(act, t) : __match_any_sync(act, key);
-          const int leader = __ffs(peers) - 1;
-          int slot = 0;
-          if (lane == leader) {
-            const unsigned long long k16 = static_cast<unsigned long long>(__popc(peers)) << 16;
-            uint32_t s = (n == 1) ? (tok_hash(t) >> (32 - cap_log2)) : fib_slot(key, cap_log2);
-            const unsigned long long mine = (static_cast<unsigned long long>(n == 1 ? j : key) << 32) | k16;
-            while (true) {
-              unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&ent[s]);
-              if (e == kEmpty) {
-                const unsigned long long old = atomicCAS(&ent[s], kEmpty, mine);
-                if (old == kEmpty) break;
-                e = old;
-              }
-              const uint32_t ek = static_cast<uint32_t>(e >> 32);
-              if (n == 1 ? tok[ek] == t : ek == key) {
-                atomicAdd(&ent[s], k16);
-                break;
-              }
-              s = (s + 1) & mask;
-            }
-            slot = static_cast<int>(s);
-          }
-          slot = __shfl_sync(peers, slot, leader);
-          idn[j] = static_cast<uint16_t>(slot);
-          if (n == 1) id1[j] = static_cast<uint16_t>(slot);
-        }
+
+    // ================= order 1: tokens =================
+    {
+      // P1 round 1: every candidate position stores itself into its token's home slot
+      for (int j = tid; j < clen; j += kThreads) {
+        const uint32_t home = tok_hash32(tok[j]) >> hshift;
+        ent[home] = (static_cast<uint32_t>(j) << 16) | 1u;
       }
       __syncthreads();
-      // ---- (b) reference n-grams: look up, count, max-fold (R > 1), clip
-      unsigned int hits = 0;
+      // P1 round 2: winners own their slot; equal tokens count; collisions probe
+      for (int j = tid; j < clen; j += kThreads) {
+        const T t = tok[j];
+        const uint32_t home = tok_hash32(t) >> hshift;
+        uint32_t slot = home;
+        const uint32_t w = ent[home] >> 16;
+        if (w != static_cast<uint32_t>(j)) {
+          if (tok[w] == t)
+            atomicAdd(&ent[home], 1u);
+          else
+            slot = table_insert_loser(ent, home, bmask, (static_cast<uint32_t>(j) << 16) | 1u,
+                                      [&](uint32_t x) { return tok[x] == t; });
+        }
+        id1[j] = static_cast<uint16_t>(slot);
+        idn[j] = static_cast<uint16_t>(slot);
+      }
+      __syncthreads();
+      TB_MARK(3);
+      // P2: reference tokens
       for (int r = 0; r < R; ++r) {
         const int off = s_pos[1 + r];
-        const int cnt = static_cast<int>(s_len[1 + r]) - n + 1;
-        for (int base = 0; base < cnt; base += kThreads) {
-          const int j = base + tid;
-          const int q = off + j;
-          bool el = j < cnt;
-          uint32_t key = 0;
-          T t = 0;
-          if (el) {
-            if (n == 1) {
-              t = tok[q];
-            } else {
-              el = live[q] >= n - 1 && live[q + n - 1] >= 1;
-              key = (static_cast<uint32_t>(idn[q]) << 16) | id1[q + n - 1];
-            }
-          }
-          const unsigned act = __ballot_sync(kFull, el);
-          if (!el) {
-            if (n == 1 && j < cnt) live[q] = 0;
-            continue;
-          }
-          const unsigned peers = (n == 1) ? __match_any_sync(act, t) : __match_any_sync(act, key);
-          const int leader = __ffs(peers) - 1;
+        const int rlen = static_cast<int>(s_len[1 + r]);
+        uint16_t* lrout = lrbase + rtot + p.ref_off[r];  // parity 1
+        for (int base = 0; base < rlen; base += kThreads) {
+          const int i = base + tid;
+          const int q = off + i;
           int slot = -1;
-          if (lane == leader) {
-            uint32_t s = (n == 1) ? (tok_hash(t) >> (32 - cap_log2)) : fib_slot(key, cap_log2);
-            while (true) {
-              const unsigned long long e = ent[s];
-              if (e == kEmpty) break;
-              const uint32_t ek = static_cast<uint32_t>(e >> 32);
-              if (n == 1 ? tok[ek] == t : ek == key) {
-                slot = static_cast<int>(s);
-                break;
-              }
-              s = (s + 1) & mask;
-            }
+          if (i < rlen) {
+            const T t = tok[q];
+            slot = table_find(ent, tok_hash32(t) >> hshift, bmask, [&](uint32_t x) { return tok[x] == t; });
             if (slot >= 0) {
-              const unsigned k = __popc(peers);
-              const unsigned long long old = atomicAdd(&ent[slot], static_cast<unsigned long long>(k));
-              if (R == 1) {
-                const unsigned x = static_cast<unsigned>(old & 0xffff);
-                const unsigned c = static_cast<unsigned>((old >> 16) & 0xffff);
-                const unsigned avail = c > x ? c - x : 0;
-                hits += avail < k ? avail : k;
-              }
+              xc_add(xcw, slot);
+              id1[q] = static_cast<uint16_t>(slot);
+              idn[q] = static_cast<uint16_t>(slot);
             }
+            live[q] = slot >= 0 ? 1 : 0;
           }
-          slot = __shfl_sync(peers, slot, leader);
-          if (slot >= 0) {
-            idn[q] = static_cast<uint16_t>(slot);
-            if (n == 1) id1[q] = static_cast<uint16_t>(slot);
-            live[q] = static_cast<uint8_t>(n);
-          } else if (n == 1) {
-            live[q] = 0;
-          }
-        }
-        if (R > 1) {
-          __syncthreads();
-          // fold reference r: m = max(m, x); numerator += min(c, m_new) - min(c, m_old)
-          for (uint32_t s = tid; s < cap; s += kThreads) {
-            const unsigned long long e = ent[s];
-            if (e == kEmpty) continue;
-            const unsigned x = static_cast<unsigned>(e & 0xffff);
-            if (!x) continue;
-            const unsigned c = static_cast<unsigned>((e >> 16) & 0xffff);
-            const unsigned m = mref[s];
-            if (x > m) {
-              hits += (c < x ? c : x) - (c < m ? c : m);
-              mref[s] = static_cast<uint16_t>(x);
-            }
-            ent[s] = e & ~0xffffull;
-          }
+          list_append(lrout, &s_nlr[1][r], slot >= 0, q);
         }
         __syncthreads();
+        if (R > 1) {
+          const int nf = s_nlr[1][r];
+          for (int i = tid; i < nf; i += kThreads) {
+            const int s = id1[lrout[i]];
+            const uint32_t x = xc_take(xcw, s);
+            if (x > mref[s]) mref[s] = static_cast<uint16_t>(x);
+          }
+          __syncthreads();
+        }
+      }
+      TB_MARK(4);
+      // P3: candidate liveness + clipped count (added once per slot by its owner)
+      unsigned int hits = 0;
+      for (int base = 0; base < clen; base += kThreads) {
+        const int j = base + tid;
+        bool ok = false;
+        if (j < clen) {
+          const int s = id1[j];
+          const uint32_t e = ent[s];
+          const uint32_t m = (R == 1) ? xc_get(xcw, s) : mref[s];
+          ok = m != 0;
+          if ((e >> 16) == static_cast<uint32_t>(j)) {
+            const uint32_t c = e & 0xffffu;
+            hits += c < m ? c : m;
+          }
+          live[j] = ok ? 1 : 0;
+        }
+        list_append(lc, &s_nlc[1], ok, j);
       }
       hits = __reduce_add_sync(kFull, hits);
-      if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
-      // ---- (c) candidate liveness: does the n-gram occur in some reference?
+      if (lane == 0 && hits) atomicAdd(&s_hits[0], hits);
+      __syncthreads();
+      TB_MARK(5);
+    }
+
+    // ================= orders n >= 2: packed (prefix slot, last-token slot) keys =================
+    for (int n = 2; n <= N; ++n) {
+      const int par = n & 1;
+      const int nlive = s_nlc[par ^ 1];
+      if (nlive == 0) break;  // no candidate (n-1)-gram matched: orders >= n have no hits
+      // P0: clear the slots used at order n-1, compute this order's candidate keys
       {
-        const int cnt = clen - n + 1;
-        unsigned int nlive = 0;
-        for (int j = tid; j < cnt; j += kThreads) {
-          bool el = true;
-          if (n > 1) el = live[j] >= n - 1 && live[j + n - 1] >= 1;
-          bool ok = false;
-          if (el) {
-            const int s = idn[j];
-            ok = (R == 1) ? ((ent[s] & 0xffff) != 0) : (mref[s] != 0);
-          }
-          if (ok) {
-            live[j] = static_cast<uint8_t>(n);
-            ++nlive;
-          } else if (n == 1) {
-            live[j] = 0;
-          }
+        const int cnt = n == 2 ? clen : s_nins[par ^ 1];
+        for (int i = tid; i < cnt; i += kThreads) {
+          const int s = n == 2 ? id1[i] : idn[lins[i]];
+          ent[s] = ~0u;
+          reinterpret_cast<uint16_t*>(xcw)[s] = 0;  // half-word s of the paired counts
+          if (R > 1) mref[s] = 0;
         }
-        nlive = __reduce_add_sync(kFull, nlive);
-        if (lane == 0 && nlive) atomicAdd(&s_live, static_cast<int>(nlive));
+        for (int i = tid; i < nlive; i += kThreads) {
+          const int j = lc[i];
+          const bool el = j + n - 1 < clen && live[j + n - 1] >= 1;
+          kc[j] = el ? ((static_cast<uint32_t>(idn[j]) << 16) | id1[j + n - 1]) : ~0u;
+        }
+        if (tid == 0) s_nins[par] = 0;
+        if (tid < R) s_nlr[par][tid] = 0;
+        __syncthreads();
+      }
+      // P1 round 1
+      for (int i = tid; i < nlive; i += kThreads) {
+        const int j = lc[i];
+        const uint32_t key = kc[j];
+        if (key != ~0u) ent[(key * 0x9E3779B1u) >> hshift] = (static_cast<uint32_t>(j) << 16) | 1u;
       }
       __syncthreads();
+      // P1 round 2 (+ inserted list)
+      for (int base = 0; base < nlive; base += kThreads) {
+        const int i = base + tid;
+        int j = 0;
+        bool el = false;
+        if (i < nlive) {
+          j = lc[i];
+          const uint32_t key = kc[j];
+          el = key != ~0u;
+          if (el) {
+            const uint32_t home = (key * 0x9E3779B1u) >> hshift;
+            uint32_t slot = home;
+            const uint32_t w = ent[home] >> 16;
+            if (w != static_cast<uint32_t>(j)) {
+              if (kc[w] == key)
+                atomicAdd(&ent[home], 1u);
+              else
+                slot = table_insert_loser(ent, home, bmask, (static_cast<uint32_t>(j) << 16) | 1u,
+                                          [&](uint32_t x) { return kc[x] == key; });
+            }
+            idn[j] = static_cast<uint16_t>(slot);
+          }
+        }
+        list_append(lins, &s_nins[par], el, j);
+      }
+      if (tid == 0) s_nlc[par] = 0;  // lc is consumed; it is rebuilt in P3
+      __syncthreads();
+      // P2: live reference positions
+      for (int r = 0; r < R; ++r) {
+        const int off = s_pos[1 + r];
+        const int rlen = static_cast<int>(s_len[1 + r]);
+        uint16_t* lrin = lrbase + (par ^ 1) * rtot + p.ref_off[r];
+        uint16_t* lrout = lrbase + par * rtot + p.ref_off[r];
+        const int cnt = s_nlr[par ^ 1][r];
+        for (int base = 0; base < cnt; base += kThreads) {
+          const int i = base + tid;
+          int q = 0;
+          int slot = -1;
+          if (i < cnt) {
+            q = lrin[i];
+            if (q - off + n - 1 < rlen && live[q + n - 1] >= 1) {
+              const uint32_t key = (static_cast<uint32_t>(idn[q]) << 16) | id1[q + n - 1];
+              slot = table_find(ent, (key * 0x9E3779B1u) >> hshift, bmask, [&](uint32_t x) { return kc[x] == key; });
+              if (slot >= 0) {
+                xc_add(xcw, slot);
+                idn[q] = static_cast<uint16_t>(slot);
+                live[q] = static_cast<uint8_t>(n);
+              }
+            }
+          }
+          list_append(lrout, &s_nlr[par][r], slot >= 0, q);
+        }
+        __syncthreads();
+        if (R > 1) {
+          const int nf = s_nlr[par][r];
+          for (int i = tid; i < nf; i += kThreads) {
+            const int s = idn[lrout[i]];
+            const uint32_t x = xc_take(xcw, s);
+            if (x > mref[s]) mref[s] = static_cast<uint16_t>(x);
+          }
+          __syncthreads();
+        }
+      }
+      // P3
+      {
+        const int cnt = s_nins[par];
+        unsigned int hits = 0;
+        for (int base = 0; base < cnt; base += kThreads) {
+          const int i = base + tid;
+          bool ok = false;
+          int j = 0;
+          if (i < cnt) {
+            j = lins[i];
+            const int s = idn[j];
+            const uint32_t e = ent[s];
+            const uint32_t m = (R == 1) ? xc_get(xcw, s) : mref[s];
+            ok = m != 0;
+            if ((e >> 16) == static_cast<uint32_t>(j)) {
+              const uint32_t c = e & 0xffffu;
+              hits += c < m ? c : m;
+            }
+            if (ok) live[j] = static_cast<uint8_t>(n);
+          }
+          list_append(lc, &s_nlc[par], ok, j);
+        }
+        hits = __reduce_add_sync(kFull, hits);
+        if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+      }
+      __syncthreads();
+      TB_MARK(3 + 4 * (n - 1) + 3);
     }
 
     // ---- epilogue (warp 0)
@@ -919,8 +1092,417 @@ __global__ void __launch_bounds__(kThreads, 4)
       }
     }
     __syncthreads();
+    TB_MARK(30);
+    if (b + gridDim.x < p.batch) issue_stage(b + gridDim.x);
   }
   finish_cta(p, s_tot, s_flags, s_last);
+  TB_MARK(31);
+}
+
+// --------------------------------------------------------------------------
+// Single-reference kernel (R == 1, the headline configuration).
+//
+// Candidate AND reference n-grams are inserted into one table, so there is no
+// separate lookup phase.  Insertion is store-then-verify:
+//   round 1: every position stores itself (u16) into its key's home slot —
+//            plain stores, one wins;
+//   round 2: the winner owns the slot (its own occurrence is counted
+//            implicitly); an equal key adds one to its side's count (the only
+//            atomic of the common path); a different key probes 8-slot
+//            buckets (one 16-byte load each) and CAS-inserts.
+// Per slot: owner position (u16) and one u32 word [ref count 16 | cand count 16]
+// excluding the owner.  The liveness pass adds min(cand, ref) once per slot
+// (by its owner) and keeps the positions whose n-gram occurs on the other
+// side; only those are extended at the next order (exact, see above).
+// Order-n keys live in `kc`, which aliases the token buffer (dead after order 1).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ bool cas16(uint16_t* a, uint16_t desired, uint16_t* seen) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(3));
+  const int sh = static_cast<int>((reinterpret_cast<uintptr_t>(a) & 2) * 8);
+  uint32_t cur = *reinterpret_cast<volatile uint32_t*>(w);
+  while (true) {
+    const uint16_t h = static_cast<uint16_t>(cur >> sh);
+    if (h != 0xffffu) {
+      *seen = h;
+      return false;
+    }
+    const uint32_t nw = (cur & ~(0xffffu << sh)) | (static_cast<uint32_t>(desired) << sh);
+    const uint32_t prev = atomicCAS(w, cur, nw);
+    if (prev == cur) return true;
+    cur = prev;
+  }
+}
+
+// Deferred insert of a position whose home slot was won by a different key:
+// linear probing from the home slot (8 slots per 16-byte read).  All plain
+// round-1 stores are complete, so entries are EMPTY or owned; CAS claims an
+// EMPTY one, an equal key adds to its owner's count.
+template <typename EqF>
+__device__ __forceinline__ uint32_t pair_insert_loser(uint16_t* own, uint32_t* cnt, uint32_t home, uint32_t mask,
+                                                      uint16_t me, uint32_t inc, EqF eq) {
+  uint32_t s = (home + 1) & mask;
+  while (true) {
+    const uint32_t bk = s >> 3;
+    uint4 q;
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                 : "r"(smem_u32(own + 8 * bk)));
+    const uint32_t wds[4] = {q.x, q.y, q.z, q.w};
+    for (uint32_t k = s & 7; k < 8; ++k) {
+      uint16_t v = static_cast<uint16_t>(wds[k >> 1] >> ((k & 1) * 16));
+      const uint32_t slot = 8 * bk + k;
+      if (v == 0xffffu) {
+        if (cas16(&own[slot], me, &v)) return slot;
+      }
+      if (eq(v)) {
+        atomicAdd(&cnt[v], inc);
+        return slot;
+      }
+    }
+    s = (8 * bk + 8) & mask;
+  }
+}
+
+// Per-warp segmented position lists: each warp appends to its own segment with
+// ballot + popc (no shared atomics); lane 0 publishes the segment length.
+struct WarpList {
+  uint16_t* base;  // 8 segments of `seg` entries
+  int seg;
+  int n;           // this warp's count (warp-uniform)
+  __device__ __forceinline__ void append(bool pred, int val) {
+    const unsigned m = __ballot_sync(kFull, pred);
+    const int lane = threadIdx.x & 31;
+    if (pred) base[(threadIdx.x >> 5) * seg + n + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(val);
+    n += __popc(m);
+  }
+  __device__ __forceinline__ void publish(int* counts) {
+    if ((threadIdx.x & 31) == 0) counts[threadIdx.x >> 5] = n;
+  }
+};
+
+// flat index over a segmented list -> entry (prefix sums of the 8 segment lengths)
+struct SegIndex {
+  int pre[kThreads / 32 + 1];
+  __device__ __forceinline__ void init(const int* counts) {
+    pre[0] = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) pre[w + 1] = pre[w] + counts[w];
+  }
+  __device__ __forceinline__ int total() const { return pre[kThreads / 32]; }
+  __device__ __forceinline__ int at(const uint16_t* base, int seg, int i) const {
+    int w = 0, off = 0;
+#pragma unroll
+    for (int k = 1; k < kThreads / 32; ++k)
+      if (i >= pre[k]) {
+        w = k;
+        off = pre[k];
+      }
+    return base[w * seg + (i - off)];
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 4)
+    bleu_pair_kernel(const __grid_constant__ StatsParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int s_hits[TB_MAX_ORDER];
+  __shared__ int64_t s_len[2];
+  __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
+  __shared__ int s_last, s_flags;
+  __shared__ int s_cnt_live[2][kThreads / 32];
+  __shared__ int s_cnt_lost[kThreads / 32];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int N = p.max_order;
+  const int cap_log2 = p.cap_log2;
+  const uint32_t cap = 1u << cap_log2;
+  const bool corpus = p.totals != nullptr || p.corpus != nullptr;
+  const int cpad = p.cand_pad;
+  const int roff = cpad;  // first reference position
+  const int seg = p.off_seg;  // entries per warp segment
+
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  T* tok = reinterpret_cast<T*>(smem + 16);
+  uint32_t* kc = reinterpret_cast<uint32_t*>(smem + 16);           // aliases tok (orders >= 2)
+  uint16_t* id1 = reinterpret_cast<uint16_t*>(smem + p.off_id1);   // order-1 slot; 0xffff: token unmatched
+  uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot
+  uint16_t* own = reinterpret_cast<uint16_t*>(smem + p.off_ent);   // slot -> owner position, 0xffff = empty
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + p.off_mref);  // owner -> [ref 16 | cand 16], owner excluded
+  uint16_t* lists = reinterpret_cast<uint16_t*>(smem + p.off_lists);
+  auto live_l = [&](int par) { return lists + par * 8 * seg; };
+  uint16_t* lost_l = lists + 16 * seg;
+  const uint32_t hshift = 32 - cap_log2;
+  const uint32_t mask = cap - 1;
+  const T* cand_g = static_cast<const T*>(p.cand_ids);
+  const T* ref_g = static_cast<const T*>(p.refs[0].ids);
+
+  auto issue_stage = [&](int64_t b) {
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      const T* srcs[2] = {cand_g + b * p.cand_ld, ref_g + b * p.refs[0].ld};
+      const int64_t ws[2] = {p.cand_width, p.refs[0].width};
+      uint32_t total = 0;
+      for (int s = 0; s < 2; ++s)
+        if ((reinterpret_cast<uintptr_t>(srcs[s]) & 15) == 0) total += static_cast<uint32_t>((ws[s] * sizeof(T)) & ~int64_t(15));
+      mbar_arrive_expect_tx(mbar, total);
+      for (int s = 0; s < 2; ++s) {
+        const uint32_t bytes = static_cast<uint32_t>((ws[s] * sizeof(T)) & ~int64_t(15));
+        if ((reinterpret_cast<uintptr_t>(srcs[s]) & 15) == 0 && bytes > 0)
+          bulk_g2s(tok + (s == 0 ? 0 : roff), srcs[s], bytes, mbar);
+      }
+    }
+  };
+
+  if (tid < 2 * N + 2) s_tot[tid] = 0;
+  if (tid == 0) {
+    s_flags = 0;
+    mbar_init(mbar, 1);
+  }
+  if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
+  __syncthreads();
+  TB_MARK(0);
+  uint32_t phase = 0;
+
+  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    if (tid < 2) {
+      const int64_t len = tid == 0 ? p.cand_len[b] : p.refs[0].len[b];
+      const int64_t width = tid == 0 ? p.cand_width : p.refs[0].width;
+      int64_t l = len;
+      if (len < 0 || len > width) {
+        atomicOr(&s_flags, TB_FLAG_BAD_LENGTH);
+        l = len < 0 ? 0 : width;
+      }
+      s_len[tid] = l;
+    }
+    if (tid < N) s_hits[tid] = 0;
+    for (int s = 0; s < 2; ++s) {  // tails / unaligned rows
+      const T* src = s == 0 ? cand_g + b * p.cand_ld : ref_g + b * p.refs[0].ld;
+      const int64_t w = s == 0 ? p.cand_width : p.refs[0].width;
+      const int64_t start = ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
+                                ? static_cast<int64_t>(((w * sizeof(T)) & ~int64_t(15)) / sizeof(T))
+                                : 0;
+      T* dst = tok + (s == 0 ? 0 : roff);
+      for (int64_t j = start + tid; j < w; j += kThreads) dst[j] = src[j];
+    }
+    for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    __syncthreads();
+    TB_MARK(2);
+
+    const int clen = static_cast<int>(s_len[0]);
+    const int rlen = static_cast<int>(s_len[1]);
+    const int tot = clen + rlen;
+    auto posof = [&](int i) { return i < clen ? i : roff + (i - clen); };
+
+    // ================= order 1: tokens =================
+    for (int i = tid; i < tot; i += kThreads) {
+      const int pos = posof(i);
+      own[tok_hash32(tok[pos]) >> hshift] = static_cast<uint16_t>(pos);
+      cnt[pos] = 0;
+    }
+    __syncthreads();
+    {
+      WarpList lost{lost_l, seg, 0};
+      for (int base = 0; base < tot; base += kThreads) {
+        const int i = base + tid;
+        bool l = false;
+        int pos = 0;
+        if (i < tot) {
+          pos = posof(i);
+          const T t = tok[pos];
+          const uint32_t home = tok_hash32(t) >> hshift;
+          const uint16_t w = own[home];
+          if (w != pos) {
+            if (tok[w] == t)
+              atomicAdd(&cnt[w], pos < roff ? 1u : (1u << 16));
+            else
+              l = true;
+          }
+          id1[pos] = static_cast<uint16_t>(home);
+        }
+        lost.append(l, pos);
+      }
+      lost.publish(s_cnt_lost);
+      if (__syncthreads_or(lost.n > 0)) {  // deferred inserts, compacted
+        SegIndex ix;
+        ix.init(s_cnt_lost);
+        for (int i = tid; i < ix.total(); i += kThreads) {
+          const int pos = ix.at(lost_l, seg, i);
+          const T t = tok[pos];
+          id1[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, id1[pos], mask, static_cast<uint16_t>(pos),
+                                                             pos < roff ? 1u : (1u << 16),
+                                                             [&](uint16_t x) { return tok[x] == t; }));
+        }
+        __syncthreads();
+      }
+    }
+    TB_MARK(3);
+    int nlive;
+    {
+      unsigned int hits = 0;
+      bool live_c = false;
+      WarpList out{live_l(1), seg, 0};
+      for (int base = 0; base < tot; base += kThreads) {
+        const int i = base + tid;
+        bool ok = false;
+        int pos = 0;
+        if (i < tot) {
+          pos = posof(i);
+          const int s = id1[pos];
+          const uint32_t o = own[s];
+          const uint32_t cw = cnt[o];
+          const uint32_t c = (cw & 0xffffu) + (o < static_cast<uint32_t>(roff) ? 1u : 0u);
+          const uint32_t x = (cw >> 16) + (o >= static_cast<uint32_t>(roff) ? 1u : 0u);
+          ok = pos < roff ? x != 0 : c != 0;
+          if (o == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
+          const uint16_t v = ok ? static_cast<uint16_t>(s) : static_cast<uint16_t>(0xffffu);
+          id1[pos] = v;  // token unmatched: no n-gram can contain it
+          idn[pos] = v;
+          live_c |= ok && pos < roff;
+        }
+        out.append(ok, pos);
+      }
+      out.publish(s_cnt_live[1]);
+      hits = __reduce_add_sync(kFull, hits);
+      if (lane == 0 && hits) atomicAdd(&s_hits[0], hits);
+      nlive = __syncthreads_count(live_c);
+    }
+    TB_MARK(4);
+
+    // ================= orders n >= 2: live positions only =================
+    for (int n = 2; n <= N && nlive; ++n) {
+      const int par = n & 1;
+      const uint16_t* lin = live_l(par ^ 1);
+      SegIndex ix;
+      ix.init(s_cnt_live[par ^ 1]);
+      const int tot_n = ix.total();
+      // P0: clear the table; keys (prefix slot, last-token slot) of eligible positions
+      for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      for (int i = tid; i < tot_n; i += kThreads) {
+        const int pos = ix.at(lin, seg, i);
+        const int end = pos < roff ? clen : roff + rlen;
+        const int q = pos + n - 1;
+        uint32_t key = ~0u;
+        if (q < end) {
+          const uint16_t last = id1[q];
+          if (last != 0xffffu) key = (static_cast<uint32_t>(idn[pos]) << 16) | last;
+        }
+        kc[pos] = key;
+        cnt[pos] = 0;
+      }
+      __syncthreads();
+      for (int i = tid; i < tot_n; i += kThreads) {
+        const int pos = ix.at(lin, seg, i);
+        const uint32_t key = kc[pos];
+        if (key != ~0u) own[(key * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(pos);
+      }
+      __syncthreads();
+      {
+        WarpList lost{lost_l, seg, 0};
+        for (int base = 0; base < tot_n; base += kThreads) {
+          const int i = base + tid;
+          bool l = false;
+          int pos = 0;
+          if (i < tot_n) {
+            pos = ix.at(lin, seg, i);
+            const uint32_t key = kc[pos];
+            if (key != ~0u) {
+              const uint32_t home = (key * 0x9E3779B1u) >> hshift;
+              const uint16_t w = own[home];
+              if (w != pos) {
+                if (kc[w] == key)
+                  atomicAdd(&cnt[w], pos < roff ? 1u : (1u << 16));
+                else
+                  l = true;
+              }
+              idn[pos] = static_cast<uint16_t>(home);
+            }
+          }
+          lost.append(l, pos);
+        }
+        lost.publish(s_cnt_lost);
+        if (__syncthreads_or(lost.n > 0)) {
+          SegIndex lx;
+          lx.init(s_cnt_lost);
+          for (int i = tid; i < lx.total(); i += kThreads) {
+            const int pos = lx.at(lost_l, seg, i);
+            const uint32_t key = kc[pos];
+            idn[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, idn[pos], mask, static_cast<uint16_t>(pos),
+                                                               pos < roff ? 1u : (1u << 16),
+                                                               [&](uint16_t x) { return kc[x] == key; }));
+          }
+          __syncthreads();
+        }
+      }
+      {
+        unsigned int hits = 0;
+        bool live_c = false;
+        WarpList out{live_l(par), seg, 0};
+        for (int base = 0; base < tot_n; base += kThreads) {
+          const int i = base + tid;
+          bool ok = false;
+          int pos = 0;
+          if (i < tot_n) {
+            pos = ix.at(lin, seg, i);
+            if (kc[pos] != ~0u) {
+              const uint32_t o = own[idn[pos]];
+              const uint32_t cw = cnt[o];
+              const uint32_t c = (cw & 0xffffu) + (o < static_cast<uint32_t>(roff) ? 1u : 0u);
+              const uint32_t x = (cw >> 16) + (o >= static_cast<uint32_t>(roff) ? 1u : 0u);
+              ok = pos < roff ? x != 0 : c != 0;
+              if (o == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
+            }
+            live_c |= ok && pos < roff;
+          }
+          out.append(ok, pos);
+        }
+        out.publish(s_cnt_live[par]);
+        hits = __reduce_add_sync(kFull, hits);
+        if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+        nlive = __syncthreads_count(live_c);
+      }
+      TB_MARK(3 + 4 * (n - 1) + 3);
+    }
+
+    // ---- epilogue (warp 0)
+    if (tid < 32) {
+      const int64_t c = s_len[0];
+      const int64_t num = lane < N ? static_cast<int64_t>(s_hits[lane]) : 0;
+      const int64_t den = (lane < N && c - lane > 0) ? c - lane : 0;
+      if (lane < N) {
+        if (p.num) p.num[b * N + lane] = num;
+        if (p.den) p.den[b * N + lane] = den;
+      }
+      const int64_t r = s_len[1];
+      if (lane == 0) {
+        if (p.cand_len_out) p.cand_len_out[b] = c;
+        if (p.eff_ref) p.eff_ref[b] = r;
+      }
+      if (p.scores || p.precisions || p.bp)
+        warp_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, lane < N ? p.weights[lane] : 0.0,
+                      p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
+                      p.scores ? p.scores + b : nullptr);
+      if (corpus) {
+        if (lane < N) {
+          s_tot[lane] += static_cast<unsigned long long>(num);
+          s_tot[N + lane] += static_cast<unsigned long long>(den);
+        }
+        if (lane == 0) {
+          s_tot[2 * N] += static_cast<unsigned long long>(c);
+          s_tot[2 * N + 1] += static_cast<unsigned long long>(r);
+        }
+      }
+    }
+    if (b + gridDim.x < p.batch) {
+      __syncthreads();
+      issue_stage(b + gridDim.x);
+    }
+    TB_MARK(30);
+  }
+  finish_cta(p, s_tot, s_flags, s_last);
+  TB_MARK(31);
 }
 
 // --------------------------------------------------------------------------
@@ -1032,10 +1614,11 @@ int dev_info(DevInfo** out) {
 // --------------------------------------------------------------------------
 struct Plan {
   bool smem_mode = false;
+  bool pair = false;  // single-reference kernel
   int cap_log2 = 0;
   int cand_pad = 0;
   int ref_off[TB_MAX_REFS + 1] = {0};
-  int off_id1 = 0, off_idn = 0, off_live = 0, off_ent = 0, off_mref = 0;
+  int off_id1 = 0, off_idn = 0, off_live = 0, off_ent = 0, off_mref = 0, off_kc = 0, off_lists = 0, off_seg = 0;
   size_t smem_bytes = 0;   // dynamic smem (smem mode)
   size_t gtab_stride = 0;  // per-CTA table bytes (global mode)
   int64_t grid = 0;
@@ -1067,8 +1650,56 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
   const int64_t elems16 = 16 / token_bytes;
   pl->acc_bytes = kAccBytes;
 
-  // ---- shared-memory (pruned progressive) layout
+  // ---- single reference: joint-insert kernel
   pl->cand_pad = static_cast<int>(round_up(cand_width, elems16));
+  if (R == 1) {
+    const int64_t rpad = round_up(ref_widths[0], elems16);
+    const int64_t ptot = pl->cand_pad + rpad;
+    // a warp appends at most 32 entries per scan step over the group's positions
+    const int64_t seg = 32 * ((ptot + kThreads - 1) / kThreads);
+    auto pair_layout = [&](int log2, int64_t* offs) {
+      const int64_t c = int64_t(1) << log2;
+      int64_t o = round_up(16 + ptot * (token_bytes > 4 ? token_bytes : 4), 16);
+      offs[0] = o;                       // id1
+      o = round_up(o + ptot * 2, 16);
+      offs[1] = o;                       // idn
+      o = round_up(o + ptot * 2, 16);
+      offs[2] = o;                       // own (u16 per slot)
+      o = round_up(o + c * 2, 16);
+      offs[3] = o;                       // cnt (u32 per position)
+      o = round_up(o + ptot * 4, 16);
+      offs[4] = o;                       // lists: live x2, lost; 8 warp segments of `seg` each
+      o = round_up(o + 3 * 8 * seg * 2, 16);
+      offs[5] = o;
+      return o;
+    };
+    // table load factor <= 1/4 when four CTAs still fit per SM, else <= 1/2
+    int lg = cap_log2_for(4 * ptot, 6);
+    int64_t offs[6];
+    int64_t total = pair_layout(lg, offs);
+    while (total + static_cast<int64_t>(kStaticSmemReserve) > smem_optin / 4 && (int64_t(1) << (lg - 1)) >= 2 * ptot) {
+      --lg;
+      total = pair_layout(lg, offs);
+    }
+    if (lg <= 16 && ptot <= 16384 && total + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin) {
+      pl->smem_mode = true;
+      pl->pair = true;
+      pl->cap_log2 = lg;
+      pl->ref_off[0] = 0;
+      pl->ref_off[1] = static_cast<int>(rpad);
+      pl->off_id1 = static_cast<int>(offs[0]);
+      pl->off_idn = static_cast<int>(offs[1]);
+      pl->off_ent = static_cast<int>(offs[2]);
+      pl->off_mref = static_cast<int>(offs[3]);
+      pl->off_lists = static_cast<int>(offs[4]);
+      pl->off_seg = static_cast<int>(seg);
+      pl->smem_bytes = static_cast<size_t>(total);
+      pl->ws_bytes = pl->acc_bytes;
+      return TB_OK;
+    }
+  }
+
+  // ---- shared-memory (pruned progressive) layout
   int64_t off = 0;
   for (int r = 0; r < R; ++r) {
     pl->ref_off[r] = static_cast<int>(off);
@@ -1076,31 +1707,47 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
   }
   pl->ref_off[R] = static_cast<int>(off);
   const int64_t ptot = pl->cand_pad + off;  // positions (candidate + references, padded)
-  const int sm_log2 = cap_log2_for(2 * cand_width, 6);
-  const int64_t sm_cap = int64_t(1) << sm_log2;
-  int64_t o = 16 + ptot * token_bytes;
-  o = round_up(o, 16);
-  const int64_t o_id1 = o;
-  o = round_up(o + ptot * 2, 16);
-  const int64_t o_idn = o;
-  o = round_up(o + ptot * 2, 16);
-  const int64_t o_live = o;
-  o = round_up(o + ptot, 16);
-  const int64_t o_ent = o;
-  o = round_up(o + sm_cap * 8, 16);
-  const int64_t o_mref = o;
-  if (R > 1) o = round_up(o + sm_cap * 2, 16);
-  const bool fits = cand_width <= 32768 && max_rw <= 65535 &&
-                    o + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin;
+  auto layout = [&](int log2, int64_t* offs) {
+    const int64_t c = int64_t(1) << log2;
+    int64_t o = round_up(16 + ptot * token_bytes, 16);
+    offs[0] = o;                              // id1
+    o = round_up(o + ptot * 2, 16);
+    offs[1] = o;                              // idn
+    o = round_up(o + ptot * 2, 16);
+    offs[2] = o;                              // live
+    o = round_up(o + ptot, 16);
+    offs[3] = o;                              // ent (u32) + reference counts (u16)
+    o = round_up(o + c * 6, 16);
+    offs[4] = o;                              // mref
+    if (R > 1) o = round_up(o + c * 2, 16);
+    offs[5] = o;                              // kc (u32 per candidate position)
+    o = round_up(o + static_cast<int64_t>(pl->cand_pad) * 4, 16);
+    offs[6] = o;                              // lists: lc, ins (cand_pad each), lr[2] (ref_off[R] each)
+    o = round_up(o + (2 * pl->cand_pad + 2 * off) * 2, 16);
+    return o;
+  };
+  int64_t offs[7];
+  // load factor <= 1/4 when four CTAs still fit per SM, else <= 1/2
+  int sm_log2 = cap_log2_for(4 * cand_width, 6);
+  if (sm_log2 > 16) sm_log2 = 16;
+  int64_t total = layout(sm_log2, offs);
+  if (total + static_cast<int64_t>(kStaticSmemReserve) > smem_optin / 4 && sm_log2 > 6) {
+    --sm_log2;
+    total = layout(sm_log2, offs);
+  }
+  const bool fits = cand_width <= 32768 && max_rw <= 65535 && ptot <= 65535 && (int64_t(1) << sm_log2) >= 2 * cand_width &&
+                    total + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin;
   if (fits) {
     pl->smem_mode = true;
     pl->cap_log2 = sm_log2;
-    pl->off_id1 = static_cast<int>(o_id1);
-    pl->off_idn = static_cast<int>(o_idn);
-    pl->off_live = static_cast<int>(o_live);
-    pl->off_ent = static_cast<int>(o_ent);
-    pl->off_mref = static_cast<int>(o_mref);
-    pl->smem_bytes = static_cast<size_t>(o);
+    pl->off_id1 = static_cast<int>(offs[0]);
+    pl->off_idn = static_cast<int>(offs[1]);
+    pl->off_live = static_cast<int>(offs[2]);
+    pl->off_ent = static_cast<int>(offs[3]);
+    pl->off_mref = static_cast<int>(offs[4]);
+    pl->off_kc = static_cast<int>(offs[5]);
+    pl->off_lists = static_cast<int>(offs[6]);
+    pl->smem_bytes = static_cast<size_t>(total);
     pl->gtab_stride = 0;
     pl->ws_bytes = pl->acc_bytes;
     return TB_OK;
@@ -1147,6 +1794,10 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
 
 template <typename T>
 int launch_stats(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream) {
+  if (pl.pair) {
+    static size_t attr_set[64] = {0};
+    return launch_kernel(bleu_pair_kernel<T>, prm, pl, sms, true, attr_set, stream);
+  }
   if (pl.smem_mode) {
     static size_t attr_set[64] = {0};
     return launch_kernel(bleu_group_kernel<T>, prm, pl, sms, true, attr_set, stream);
@@ -1195,6 +1846,13 @@ const char* tb_strerror(int code) {
 }
 
 const char* tb_last_cuda_error(void) { return g_last_cuda_error; }
+
+#ifdef TB_PHASES
+int tb_debug_phase_buffer(void* buf) {
+  TB_CUDA(cudaMemcpyToSymbol(g_tb_phases, &buf, sizeof(buf)));
+  return TB_OK;
+}
+#endif
 
 size_t tb_bleu_workspace_bytes(int64_t batch, int32_t num_refs, int64_t cand_width,
                                const int64_t* ref_widths, int32_t token_bytes, int32_t max_order) {
@@ -1289,6 +1947,9 @@ int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, in
   prm.off_live = pl.off_live;
   prm.off_ent = pl.off_ent;
   prm.off_mref = pl.off_mref;
+  prm.off_kc = pl.off_kc;
+  prm.off_lists = pl.off_lists;
+  prm.off_seg = pl.off_seg;
   prm.gtab = pl.smem_mode ? nullptr : ws + pl.acc_bytes;
   prm.gtab_stride = pl.gtab_stride;
 

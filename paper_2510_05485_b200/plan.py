@@ -107,5 +107,8 @@ class SentenceBleuPlan:
         self.graph.replay()
 
     def check(self) -> None:
-        """Synchronise and raise if the last run flagged bad input data."""
-        _native.raise_flags(int(self.err.item()))
+        """Synchronise and raise if any run since the last check flagged bad
+        input data (the flag word is sticky: launches OR into it)."""
+        flags = int(self.err.item())
+        self.err.zero_()
+        _native.raise_flags(flags)

@@ -1,0 +1,69 @@
+"""Per-phase timing of the fused kernel (debug build with -DTB_PHASES).
+
+    python tools/phase_profile.py [--workload c2]
+
+Loads libtensorbleu_b200_phases.so instead of the product library, runs the
+workload, and prints for every phase mark the median / p90 time since the
+CTA started, plus the spread of CTA start/finish times (ns, %globaltimer)."""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2510_05485_b200 import _native  # noqa: E402
+
+_native.LIB_PATH = os.path.join(_native.PKG_DIR, "libtensorbleu_b200_phases.so")
+import paper_2510_05485_b200 as tb  # noqa: E402
+import bench  # noqa: E402
+
+NAMES = {0: "start", 1: "lengths", 2: "staged", 30: "epilogue", 31: "finish"}
+for n in range(1, 8):
+    for k, nm in enumerate(["P0clear", "P1cand", "P2ref", "P3live"]):
+        NAMES[3 + 4 * (n - 1) + k] = f"o{n}.{nm}"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--dtype", default="int32")
+    args = ap.parse_args()
+    b, l, v, r, sm = bench.WORKLOADS[args.workload]
+    (cid, clen), refs = bench.generate_batch(b, l, v, r)
+    dt = torch.int32 if args.dtype == "int32" else torch.int64
+    cand = tb.TokenBatch(ids=torch.as_tensor(cid).cuda().to(dt), lengths=torch.as_tensor(clen).cuda())
+    rb = [tb.TokenBatch(ids=torch.as_tensor(i).cuda().to(dt), lengths=torch.as_tensor(ln).cuda()) for i, ln in refs]
+    lib = _native.load()
+    lib.tb_debug_phase_buffer.argtypes = [ctypes.c_void_p]
+    buf = torch.zeros(b * 32, dtype=torch.int64, device="cuda")
+    lib.tb_debug_phase_buffer(buf.data_ptr())
+    plan = tb.SentenceBleuPlan(cand, rb, tb.BleuConfig(smoothing=sm))
+    for _ in range(5):
+        plan.run()
+    buf.zero_()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush.zero_()
+    plan.run()
+    torch.cuda.synchronize()
+    t = buf.cpu().numpy().reshape(b, 32).astype(np.int64)
+    grid = int((t[:, 0] > 0).sum())
+    t = t[:grid]
+    t0 = t[:, 0].min()
+    print(f"CTAs {grid}; CTA start spread {np.ptp(t[:, 0])} ns; first start -> last finish "
+          f"{t[:, 31].max() - t0} ns")
+    for k in range(32):
+        col = t[:, k]
+        ok = col > 0
+        if not ok.any():
+            continue
+        rel = col[ok] - t[ok, 0]
+        print(f"{NAMES.get(k, k):>12}: n={ok.sum():4d} since CTA start median {np.median(rel):8.0f} "
+              f"p90 {np.percentile(rel, 90):8.0f} max {rel.max():8.0f} ns")
+
+
+if __name__ == "__main__":
+    main()
