@@ -331,16 +331,18 @@ __device__ void warp_epilogue(int64_t num, int64_t den, int64_t c, int64_t r, in
   double bp = (cd > rd) ? 1.0 : exp(__dsub_rn(1.0, __ddiv_rn(rd, cd > 0.0 ? cd : 1.0)));
   if (!(cd > 0.0)) bp = 0.0;
   const bool wpos = act && w > 0.0;
-  const bool bad = __any_sync(kFull, wpos && !(pn > 0.0));
-  const double term = (wpos && pn > 0.0) ? __dmul_rn(log(pn), w) : 0.0;
-  double s = 0.0;
-  for (int n = 0; n < N; ++n) {
-    const double t = __shfl_sync(kFull, term, n);
-    if (__shfl_sync(kFull, wpos ? 1 : 0, n)) s = __dadd_rn(s, t);
+  const bool bad = __any_sync(kFull, wpos && !(pn > 0.0));  // an active precision is 0: score 0
+  double score = 0.0;
+  if (!bad) {
+    const double term = wpos ? __dmul_rn(log(pn), w) : 0.0;
+    double s = 0.0;
+    for (int n = 0; n < N; ++n) {
+      const double t = __shfl_sync(kFull, term, n);
+      if (__shfl_sync(kFull, wpos ? 1 : 0, n)) s = __dadd_rn(s, t);
+    }
+    score = fmin(fmax(__dmul_rn(bp, exp(s)), 0.0), 1.0);
   }
   if (lane == 0) {
-    double score = bad ? 0.0 : __dmul_rn(bp, exp(s));
-    score = fmin(fmax(score, 0.0), 1.0);
     if (bp_out) *bp_out = bp;
     if (score_out) *score_out = score;
   }
@@ -646,6 +648,16 @@ __device__ unsigned long long* g_tb_phases;
   do {             \
   } while (0)
 #endif
+#ifdef TB_PHASES
+#define TB_NOTE(k, v)                                                   \
+  do {                                                                  \
+    if (threadIdx.x == 0 && g_tb_phases) g_tb_phases[blockIdx.x * 32 + (k)] = (v); \
+  } while (0)
+#else
+#define TB_NOTE(k, v) \
+  do {                \
+  } while (0)
+#endif
 
 // 32-bit multiplicative hash of a token; use the TOP bits (h >> (32 - bits))
 template <typename T>
@@ -653,7 +665,10 @@ __device__ __forceinline__ uint32_t tok_hash32(T t) {
   if constexpr (sizeof(T) == 4) {
     return static_cast<uint32_t>(t) * 0x9E3779B1u;
   } else {
-    const uint64_t h = static_cast<uint64_t>(t) * 0x9E3779B97F4A7C15ull;
+    uint64_t h = static_cast<uint64_t>(t);
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
     return static_cast<uint32_t>(h >> 32);
   }
 }
@@ -1116,10 +1131,21 @@ __global__ void __launch_bounds__(kThreads, 4)
 // side; only those are extended at the next order (exact, see above).
 // Order-n keys live in `kc`, which aliases the token buffer (dead after order 1).
 // --------------------------------------------------------------------------
-__device__ __forceinline__ bool cas16(uint16_t* a, uint16_t desired, uint16_t* seen) {
-  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(3));
-  const int sh = static_cast<int>((reinterpret_cast<uintptr_t>(a) & 2) * 8);
-  uint32_t cur = *reinterpret_cast<volatile uint32_t*>(w);
+// 32-bit CAS on a shared-memory address (explicit state space: the address is
+// computed with integer arithmetic, which would otherwise become a generic,
+// GPU-scope ATOM instead of ATOMS).
+__device__ __forceinline__ uint32_t atom_cas_shared(uint32_t saddr, uint32_t cmp, uint32_t val) {
+  uint32_t old;
+  asm volatile("atom.shared::cta.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(saddr), "r"(cmp), "r"(val) : "memory");
+  return old;
+}
+
+// claim the EMPTY (0xffff) u16 slot `slot` of `own` for `desired`
+__device__ __forceinline__ bool cas16(uint16_t* own, uint32_t slot, uint16_t desired, uint16_t* seen) {
+  const uint32_t waddr = smem_u32(own) + 4 * (slot >> 1);
+  const int sh = static_cast<int>((slot & 1) * 16);
+  uint32_t cur;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(cur) : "r"(waddr));
   while (true) {
     const uint16_t h = static_cast<uint16_t>(cur >> sh);
     if (h != 0xffffu) {
@@ -1127,7 +1153,7 @@ __device__ __forceinline__ bool cas16(uint16_t* a, uint16_t desired, uint16_t* s
       return false;
     }
     const uint32_t nw = (cur & ~(0xffffu << sh)) | (static_cast<uint32_t>(desired) << sh);
-    const uint32_t prev = atomicCAS(w, cur, nw);
+    const uint32_t prev = atom_cas_shared(waddr, cur, nw);
     if (prev == cur) return true;
     cur = prev;
   }
@@ -1140,66 +1166,19 @@ __device__ __forceinline__ bool cas16(uint16_t* a, uint16_t desired, uint16_t* s
 template <typename EqF>
 __device__ __forceinline__ uint32_t pair_insert_loser(uint16_t* own, uint32_t* cnt, uint32_t home, uint32_t mask,
                                                       uint16_t me, uint32_t inc, EqF eq) {
+  const uint32_t base = smem_u32(own);
   uint32_t s = (home + 1) & mask;
   while (true) {
-    const uint32_t bk = s >> 3;
-    uint4 q;
-    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
-                 : "r"(smem_u32(own + 8 * bk)));
-    const uint32_t wds[4] = {q.x, q.y, q.z, q.w};
-    for (uint32_t k = s & 7; k < 8; ++k) {
-      uint16_t v = static_cast<uint16_t>(wds[k >> 1] >> ((k & 1) * 16));
-      const uint32_t slot = 8 * bk + k;
-      if (v == 0xffffu) {
-        if (cas16(&own[slot], me, &v)) return slot;
-      }
-      if (eq(v)) {
-        atomicAdd(&cnt[v], inc);
-        return slot;
-      }
+    uint16_t v;
+    asm volatile("ld.volatile.shared.u16 %0, [%1];" : "=h"(v) : "r"(base + 2 * s));
+    if (v == 0xffffu && cas16(own, s, me, &v)) return s;
+    if (eq(v)) {
+      atomicAdd(&cnt[v], inc);
+      return s;
     }
-    s = (8 * bk + 8) & mask;
+    s = (s + 1) & mask;
   }
 }
-
-// Per-warp segmented position lists: each warp appends to its own segment with
-// ballot + popc (no shared atomics); lane 0 publishes the segment length.
-struct WarpList {
-  uint16_t* base;  // 8 segments of `seg` entries
-  int seg;
-  int n;           // this warp's count (warp-uniform)
-  __device__ __forceinline__ void append(bool pred, int val) {
-    const unsigned m = __ballot_sync(kFull, pred);
-    const int lane = threadIdx.x & 31;
-    if (pred) base[(threadIdx.x >> 5) * seg + n + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(val);
-    n += __popc(m);
-  }
-  __device__ __forceinline__ void publish(int* counts) {
-    if ((threadIdx.x & 31) == 0) counts[threadIdx.x >> 5] = n;
-  }
-};
-
-// flat index over a segmented list -> entry (prefix sums of the 8 segment lengths)
-struct SegIndex {
-  int pre[kThreads / 32 + 1];
-  __device__ __forceinline__ void init(const int* counts) {
-    pre[0] = 0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) pre[w + 1] = pre[w] + counts[w];
-  }
-  __device__ __forceinline__ int total() const { return pre[kThreads / 32]; }
-  __device__ __forceinline__ int at(const uint16_t* base, int seg, int i) const {
-    int w = 0, off = 0;
-#pragma unroll
-    for (int k = 1; k < kThreads / 32; ++k)
-      if (i >= pre[k]) {
-        w = k;
-        off = pre[k];
-      }
-    return base[w * seg + (i - off)];
-  }
-};
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 4)
@@ -1209,8 +1188,8 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int64_t s_len[2];
   __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
   __shared__ int s_last, s_flags;
-  __shared__ int s_cnt_live[2][kThreads / 32];
-  __shared__ int s_cnt_lost[kThreads / 32];
+  __shared__ int s_nlost, s_nsurv;
+  __shared__ uint16_t s_surv[32];  // order-1 survivors when there are at most 32
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -1219,19 +1198,16 @@ __global__ void __launch_bounds__(kThreads, 4)
   const uint32_t cap = 1u << cap_log2;
   const bool corpus = p.totals != nullptr || p.corpus != nullptr;
   const int cpad = p.cand_pad;
-  const int roff = cpad;  // first reference position
-  const int seg = p.off_seg;  // entries per warp segment
+  const int roff = cpad;  // first reference position (multiple of 4)
 
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
   T* tok = reinterpret_cast<T*>(smem + 16);
   uint32_t* kc = reinterpret_cast<uint32_t*>(smem + 16);           // aliases tok (orders >= 2)
   uint16_t* id1 = reinterpret_cast<uint16_t*>(smem + p.off_id1);   // order-1 slot; 0xffff: token unmatched
-  uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot
+  uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot; 0xffff: n-gram unmatched
   uint16_t* own = reinterpret_cast<uint16_t*>(smem + p.off_ent);   // slot -> owner position, 0xffff = empty
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + p.off_mref);  // owner -> [ref 16 | cand 16], owner excluded
-  uint16_t* lists = reinterpret_cast<uint16_t*>(smem + p.off_lists);
-  auto live_l = [&](int par) { return lists + par * 8 * seg; };
-  uint16_t* lost_l = lists + 16 * seg;
+  uint32_t* lostq = reinterpret_cast<uint32_t*>(smem + p.off_lists);  // (quad base << 4) | lost-position mask
   const uint32_t hshift = 32 - cap_log2;
   const uint32_t mask = cap - 1;
   const T* cand_g = static_cast<const T*>(p.cand_ids);
@@ -1276,6 +1252,10 @@ __global__ void __launch_bounds__(kThreads, 4)
       s_len[tid] = l;
     }
     if (tid < N) s_hits[tid] = 0;
+    if (tid == 0) {
+      s_nlost = 0;
+      s_nsurv = 0;
+    }
     for (int s = 0; s < 2; ++s) {  // tails / unaligned rows
       const T* src = s == 0 ? cand_g + b * p.cand_ld : ref_g + b * p.refs[0].ld;
       const int64_t w = s == 0 ? p.cand_width : p.refs[0].width;
@@ -1293,160 +1273,259 @@ __global__ void __launch_bounds__(kThreads, 4)
 
     const int clen = static_cast<int>(s_len[0]);
     const int rlen = static_cast<int>(s_len[1]);
-    const int tot = clen + rlen;
-    auto posof = [&](int i) { return i < clen ? i : roff + (i - clen); };
+    // positions are processed in quads (4 consecutive positions of one row)
+    const int ncq = (clen + 3) >> 2;
+    const int nq = ncq + ((rlen + 3) >> 2);
+    // quad -> (first position, mask of valid positions)
+    auto quad = [&](int qi, int& p0) -> uint32_t {
+      int left;
+      if (qi < ncq) {
+        p0 = 4 * qi;
+        left = clen - p0;
+      } else {
+        p0 = roff + 4 * (qi - ncq);
+        left = rlen - (p0 - roff);
+      }
+      return left >= 4 ? 0xfu : ((1u << left) - 1u);
+    };
+    auto load4 = [&](int pos, T (&t)[4]) {
+      if constexpr (sizeof(T) == 4) {
+        const int4 v = *reinterpret_cast<const int4*>(tok + pos);
+        t[0] = v.x;
+        t[1] = v.y;
+        t[2] = v.z;
+        t[3] = v.w;
+      } else {
+        const longlong2 u = *reinterpret_cast<const longlong2*>(tok + pos);
+        const longlong2 v = *reinterpret_cast<const longlong2*>(tok + pos + 2);
+        t[0] = u.x;
+        t[1] = u.y;
+        t[2] = v.x;
+        t[3] = v.y;
+      }
+    };
+    auto inc_of = [&](int pos) { return pos < roff ? 1u : (1u << 16); };
 
     // ================= order 1: tokens =================
-    for (int i = tid; i < tot; i += kThreads) {
-      const int pos = posof(i);
-      own[tok_hash32(tok[pos]) >> hshift] = static_cast<uint16_t>(pos);
-      cnt[pos] = 0;
+    for (int qi = tid; qi < nq; qi += kThreads) {  // round 1: claim home slots (plain stores)
+      int p0;
+      const uint32_t vm = quad(qi, p0);
+      T t[4];
+      load4(p0, t);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (vm >> k & 1u) own[tok_hash32(t[k]) >> hshift] = static_cast<uint16_t>(p0 + k);
+      *reinterpret_cast<uint4*>(cnt + p0) = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
-    {
-      WarpList lost{lost_l, seg, 0};
-      for (int base = 0; base < tot; base += kThreads) {
-        const int i = base + tid;
-        bool l = false;
-        int pos = 0;
-        if (i < tot) {
-          pos = posof(i);
-          const T t = tok[pos];
-          const uint32_t home = tok_hash32(t) >> hshift;
-          const uint16_t w = own[home];
-          if (w != pos) {
-            if (tok[w] == t)
-              atomicAdd(&cnt[w], pos < roff ? 1u : (1u << 16));
-            else
-              l = true;
-          }
-          id1[pos] = static_cast<uint16_t>(home);
+    TB_MARK(28);
+    for (int qi = tid; qi < nq; qi += kThreads) {  // round 2: verify
+      int p0;
+      const uint32_t vm = quad(qi, p0);
+      T t[4];
+      load4(p0, t);
+      uint32_t home[4];
+      uint16_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) home[k] = tok_hash32(t[k]) >> hshift;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = own[home[k]];
+      uint32_t lm = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int pos = p0 + k;
+        if ((vm >> k & 1u) && w[k] != pos) {
+          if (tok[w[k]] == t[k])
+            atomicAdd(&cnt[w[k]], inc_of(pos));
+          else
+            lm |= 1u << k;
         }
-        lost.append(l, pos);
       }
-      lost.publish(s_cnt_lost);
-      if (__syncthreads_or(lost.n > 0)) {  // deferred inserts, compacted
-        SegIndex ix;
-        ix.init(s_cnt_lost);
-        for (int i = tid; i < ix.total(); i += kThreads) {
-          const int pos = ix.at(lost_l, seg, i);
+      *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
+      if (lm) lostq[atomicAdd(&s_nlost, 1)] = (static_cast<uint32_t>(p0) << 4) | lm;
+    }
+    __syncthreads();
+    TB_MARK(29);
+    if (s_nlost) {  // deferred inserts of positions whose home slot holds another token
+      const int nl = s_nlost;
+      for (int i = tid; i < nl; i += kThreads) {
+        const uint32_t e = lostq[i];
+        const int p0 = static_cast<int>(e >> 4);
+        for (int k = 0; k < 4; ++k) {
+          if (!(e >> k & 1u)) continue;
+          const int pos = p0 + k;
           const T t = tok[pos];
           id1[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, id1[pos], mask, static_cast<uint16_t>(pos),
-                                                             pos < roff ? 1u : (1u << 16),
-                                                             [&](uint16_t x) { return tok[x] == t; }));
+                                                             inc_of(pos), [&](uint16_t x) { return tok[x] == t; }));
         }
-        __syncthreads();
       }
+      __syncthreads();
     }
     TB_MARK(3);
-    int nlive;
-    {
+    {  // liveness + clipped count (added once per slot by its owner)
       unsigned int hits = 0;
-      bool live_c = false;
-      WarpList out{live_l(1), seg, 0};
-      for (int base = 0; base < tot; base += kThreads) {
-        const int i = base + tid;
-        bool ok = false;
-        int pos = 0;
-        if (i < tot) {
-          pos = posof(i);
-          const int s = id1[pos];
-          const uint32_t o = own[s];
-          const uint32_t cw = cnt[o];
-          const uint32_t c = (cw & 0xffffu) + (o < static_cast<uint32_t>(roff) ? 1u : 0u);
-          const uint32_t x = (cw >> 16) + (o >= static_cast<uint32_t>(roff) ? 1u : 0u);
-          ok = pos < roff ? x != 0 : c != 0;
-          if (o == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
-          const uint16_t v = ok ? static_cast<uint16_t>(s) : static_cast<uint16_t>(0xffffu);
-          id1[pos] = v;  // token unmatched: no n-gram can contain it
-          idn[pos] = v;
-          live_c |= ok && pos < roff;
-        }
-        out.append(ok, pos);
-      }
-      out.publish(s_cnt_live[1]);
-      hits = __reduce_add_sync(kFull, hits);
-      if (lane == 0 && hits) atomicAdd(&s_hits[0], hits);
-      nlive = __syncthreads_count(live_c);
-    }
-    TB_MARK(4);
-
-    // ================= orders n >= 2: live positions only =================
-    for (int n = 2; n <= N && nlive; ++n) {
-      const int par = n & 1;
-      const uint16_t* lin = live_l(par ^ 1);
-      SegIndex ix;
-      ix.init(s_cnt_live[par ^ 1]);
-      const int tot_n = ix.total();
-      // P0: clear the table; keys (prefix slot, last-token slot) of eligible positions
-      for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
-      for (int i = tid; i < tot_n; i += kThreads) {
-        const int pos = ix.at(lin, seg, i);
-        const int end = pos < roff ? clen : roff + rlen;
-        const int q = pos + n - 1;
-        uint32_t key = ~0u;
-        if (q < end) {
-          const uint16_t last = id1[q];
-          if (last != 0xffffu) key = (static_cast<uint32_t>(idn[pos]) << 16) | last;
-        }
-        kc[pos] = key;
-        cnt[pos] = 0;
-      }
-      __syncthreads();
-      for (int i = tid; i < tot_n; i += kThreads) {
-        const int pos = ix.at(lin, seg, i);
-        const uint32_t key = kc[pos];
-        if (key != ~0u) own[(key * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(pos);
-      }
-      __syncthreads();
-      {
-        WarpList lost{lost_l, seg, 0};
-        for (int base = 0; base < tot_n; base += kThreads) {
-          const int i = base + tid;
-          bool l = false;
-          int pos = 0;
-          if (i < tot_n) {
-            pos = ix.at(lin, seg, i);
-            const uint32_t key = kc[pos];
-            if (key != ~0u) {
-              const uint32_t home = (key * 0x9E3779B1u) >> hshift;
-              const uint16_t w = own[home];
-              if (w != pos) {
-                if (kc[w] == key)
-                  atomicAdd(&cnt[w], pos < roff ? 1u : (1u << 16));
-                else
-                  l = true;
-              }
-              idn[pos] = static_cast<uint16_t>(home);
+      for (int qi = tid; qi < nq; qi += kThreads) {
+        int p0;
+        const uint32_t vm = quad(qi, p0);
+        const uint2 s2 = *reinterpret_cast<const uint2*>(id1 + p0);
+        const uint32_t s[4] = {s2.x & 0xffffu, s2.x >> 16, s2.y & 0xffffu, s2.y >> 16};
+        uint32_t o[4], cw[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = own[s[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cw[k] = cnt[(vm >> k & 1u) ? o[k] : 0u];
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int pos = p0 + k;
+          v[k] = 0xffffu;
+          if (vm >> k & 1u) {
+            const uint32_t c = (cw[k] & 0xffffu) + (o[k] < static_cast<uint32_t>(roff) ? 1u : 0u);
+            const uint32_t x = (cw[k] >> 16) + (o[k] >= static_cast<uint32_t>(roff) ? 1u : 0u);
+            const bool ok = pos < roff ? x != 0 : c != 0;
+            if (o[k] == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
+            if (ok) {
+              v[k] = s[k];
+              const int j = atomicAdd(&s_nsurv, 1);  // survivors are rare on unrelated text
+              if (j < 32) s_surv[j] = static_cast<uint16_t>(pos);
             }
           }
-          lost.append(l, pos);
         }
-        lost.publish(s_cnt_lost);
-        if (__syncthreads_or(lost.n > 0)) {
-          SegIndex lx;
-          lx.init(s_cnt_lost);
-          for (int i = tid; i < lx.total(); i += kThreads) {
-            const int pos = lx.at(lost_l, seg, i);
-            const uint32_t key = kc[pos];
-            idn[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, idn[pos], mask, static_cast<uint16_t>(pos),
-                                                               pos < roff ? 1u : (1u << 16),
-                                                               [&](uint16_t x) { return kc[x] == key; }));
+        const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+        *reinterpret_cast<uint2*>(id1 + p0) = vv;  // 0xffff: token unmatched, no n-gram can contain it
+        *reinterpret_cast<uint2*>(idn + p0) = vv;
+      }
+      hits = __reduce_add_sync(kFull, hits);
+      if (lane == 0 && hits) atomicAdd(&s_hits[0], hits);
+    }
+    __syncthreads();
+    TB_MARK(4);
+    int nsurv = s_nsurv;
+
+    // ================= orders n >= 2 =================
+    if (nsurv > 0 && nsurv <= 32 && N >= 2) {
+      // Few survivors: warp 0 finishes every remaining order with match.any on the
+      // keys (no table, no block barriers).  An n-gram's id for the next order is
+      // the lowest lane holding it.
+      if (tid < 32) {
+        int pos = lane < nsurv ? s_surv[lane] : -1;
+        uint32_t pid = pos >= 0 ? idn[pos] : 0u;
+        for (int m = 2; m <= N; ++m) {
+          bool valid = pos >= 0;
+          uint32_t key = 0;
+          if (valid) {
+            const int end = pos < roff ? clen : roff + rlen;
+            const int q = pos + m - 1;
+            valid = q < end && id1[q] != 0xffffu;
+            if (valid) key = (pid << 16) | id1[q];
+          }
+          const unsigned peers = __match_any_sync(kFull, valid ? key : 0xffffffffu - lane);
+          const unsigned cm = __ballot_sync(kFull, valid && pos < roff);
+          const unsigned rm = __ballot_sync(kFull, valid && pos >= roff);
+          const unsigned c = __popc(peers & cm), x = __popc(peers & rm);
+          const int leader = __ffs(peers) - 1;
+          unsigned h = (valid && lane == leader) ? (c < x ? c : x) : 0u;
+          h = __reduce_add_sync(kFull, h);
+          if (lane == 0) s_hits[m - 1] += h;
+          const bool ok = valid && (pos < roff ? x > 0 : c > 0);
+          if (!__any_sync(kFull, ok && pos < roff)) break;
+          pos = ok ? pos : -1;
+          pid = static_cast<uint32_t>(leader);
+        }
+        __syncwarp();
+      }
+    } else if (nsurv > 32) {
+      // Many survivors: the same store-then-verify table per order, over position
+      // quads whose (n-1)-gram is still live (idn != 0xffff).
+      for (int n = 2; n <= N && nsurv; ++n) {
+        for (uint32_t s = tid; s < cap / 8; s += kThreads)
+          reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        for (int qi = tid; qi < nq; qi += kThreads) {  // keys of eligible positions
+          int p0;
+          const uint32_t vm = quad(qi, p0);
+          const int end = p0 < roff ? clen : roff + rlen;
+          uint32_t key[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int pos = p0 + k;
+            key[k] = ~0u;
+            if (vm >> k & 1u) {
+              const uint16_t pre = idn[pos];
+              const int q = pos + n - 1;
+              if (pre != 0xffffu && q < end) {
+                const uint16_t last = id1[q];
+                if (last != 0xffffu) key[k] = (static_cast<uint32_t>(pre) << 16) | last;
+              }
+            }
+          }
+          *reinterpret_cast<uint4*>(kc + p0) = make_uint4(key[0], key[1], key[2], key[3]);
+          *reinterpret_cast<uint4*>(cnt + p0) = make_uint4(0, 0, 0, 0);
+        }
+        if (tid == 0) {
+          s_nlost = 0;
+          s_nsurv = 0;
+        }
+        __syncthreads();
+        for (int qi = tid; qi < nq; qi += kThreads) {
+          int p0;
+          quad(qi, p0);
+          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + p0);
+          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (key[k] != ~0u) own[(key[k] * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(p0 + k);
+        }
+        __syncthreads();
+        for (int qi = tid; qi < nq; qi += kThreads) {
+          int p0;
+          quad(qi, p0);
+          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + p0);
+          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+          uint32_t lm = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (key[k] == ~0u) continue;
+            const int pos = p0 + k;
+            const uint32_t home = (key[k] * 0x9E3779B1u) >> hshift;
+            const uint16_t w = own[home];
+            if (w != pos) {
+              if (kc[w] == key[k])
+                atomicAdd(&cnt[w], inc_of(pos));
+              else
+                lm |= 1u << k;
+            }
+            idn[pos] = static_cast<uint16_t>(home);
+          }
+          if (lm) lostq[atomicAdd(&s_nlost, 1)] = (static_cast<uint32_t>(p0) << 4) | lm;
+        }
+        __syncthreads();
+        if (s_nlost) {
+          const int nl = s_nlost;
+          for (int i = tid; i < nl; i += kThreads) {
+            const uint32_t e = lostq[i];
+            const int p0 = static_cast<int>(e >> 4);
+            for (int k = 0; k < 4; ++k) {
+              if (!(e >> k & 1u)) continue;
+              const int pos = p0 + k;
+              const uint32_t key = kc[pos];
+              idn[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, idn[pos], mask, static_cast<uint16_t>(pos),
+                                                                 inc_of(pos), [&](uint16_t x) { return kc[x] == key; }));
+            }
           }
           __syncthreads();
         }
-      }
-      {
         unsigned int hits = 0;
         bool live_c = false;
-        WarpList out{live_l(par), seg, 0};
-        for (int base = 0; base < tot_n; base += kThreads) {
-          const int i = base + tid;
-          bool ok = false;
-          int pos = 0;
-          if (i < tot_n) {
-            pos = ix.at(lin, seg, i);
-            if (kc[pos] != ~0u) {
+        for (int qi = tid; qi < nq; qi += kThreads) {
+          int p0;
+          quad(qi, p0);
+          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + p0);
+          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int pos = p0 + k;
+            bool ok = false;
+            if (key[k] != ~0u) {
               const uint32_t o = own[idn[pos]];
               const uint32_t cw = cnt[o];
               const uint32_t c = (cw & 0xffffu) + (o < static_cast<uint32_t>(roff) ? 1u : 0u);
@@ -1454,16 +1533,15 @@ __global__ void __launch_bounds__(kThreads, 4)
               ok = pos < roff ? x != 0 : c != 0;
               if (o == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
             }
+            if (!ok) idn[pos] = 0xffffu;
             live_c |= ok && pos < roff;
           }
-          out.append(ok, pos);
         }
-        out.publish(s_cnt_live[par]);
         hits = __reduce_add_sync(kFull, hits);
         if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
-        nlive = __syncthreads_count(live_c);
+        nsurv = __syncthreads_count(live_c);
+        TB_MARK(3 + 4 * (n - 1) + 3);
       }
-      TB_MARK(3 + 4 * (n - 1) + 3);
     }
 
     // ---- epilogue (warp 0)
@@ -1653,10 +1731,9 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
   // ---- single reference: joint-insert kernel
   pl->cand_pad = static_cast<int>(round_up(cand_width, elems16));
   if (R == 1) {
-    const int64_t rpad = round_up(ref_widths[0], elems16);
-    const int64_t ptot = pl->cand_pad + rpad;
-    // a warp appends at most 32 entries per scan step over the group's positions
-    const int64_t seg = 32 * ((ptot + kThreads - 1) / kThreads);
+    const int64_t cpad4 = round_up(cand_width, 4);  // quads of positions never straddle the two rows
+    const int64_t rpad = round_up(ref_widths[0], 4);
+    const int64_t ptot = cpad4 + rpad;
     auto pair_layout = [&](int log2, int64_t* offs) {
       const int64_t c = int64_t(1) << log2;
       int64_t o = round_up(16 + ptot * (token_bytes > 4 ? token_bytes : 4), 16);
@@ -1668,8 +1745,8 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       o = round_up(o + c * 2, 16);
       offs[3] = o;                       // cnt (u32 per position)
       o = round_up(o + ptot * 4, 16);
-      offs[4] = o;                       // lists: live x2, lost; 8 warp segments of `seg` each
-      o = round_up(o + 3 * 8 * seg * 2, 16);
+      offs[4] = o;                       // lost-quad list (u32 per quad)
+      o = round_up(o + (ptot / 4) * 4, 16);
       offs[5] = o;
       return o;
     };
@@ -1684,6 +1761,7 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
     if (lg <= 16 && ptot <= 16384 && total + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin) {
       pl->smem_mode = true;
       pl->pair = true;
+      pl->cand_pad = static_cast<int>(cpad4);
       pl->cap_log2 = lg;
       pl->ref_off[0] = 0;
       pl->ref_off[1] = static_cast<int>(rpad);
@@ -1692,7 +1770,6 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       pl->off_ent = static_cast<int>(offs[2]);
       pl->off_mref = static_cast<int>(offs[3]);
       pl->off_lists = static_cast<int>(offs[4]);
-      pl->off_seg = static_cast<int>(seg);
       pl->smem_bytes = static_cast<size_t>(total);
       pl->ws_bytes = pl->acc_bytes;
       return TB_OK;
