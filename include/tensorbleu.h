@@ -127,6 +127,36 @@ int tb_bleu_stats(int32_t token_bytes,
                   int32_t* err_flag,
                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Host-buffer form of tb_bleu_stats: the blocking call the reference's
+ * `compute_stats` / `sentence_bleu` / `corpus_bleu` make on host arrays
+ * (bleu.py:173-305; the buffer bindings _ext.pyx:87-110 call the same).
+ * Same arguments and outputs as tb_bleu_stats, but
+ *  - token and length arrays may be HOST memory, pinned (page-locked:
+ *    cudaHostAlloc / torch pin_memory) or pageable, or device memory.  Pinned
+ *    token rows are read by the kernel directly over PCIe — only the valid
+ *    prefix of each row, overlapped with the counting — so there is no
+ *    separate full-width H2D copy; pageable rows (and every row when the
+ *    shape needs the global-memory kernel) are copied to device staging first;
+ *  - every non-NULL output is a HOST array; the kernel writes results into a
+ *    pinned staging area that is copied out after the stream synchronises;
+ *  - the workspace and staging buffers are owned by the library (cached per
+ *    calling thread and device);
+ *  - the call synchronises `stream` and returns the device-detected data
+ *    errors in *flags_out (TB_FLAG_* bits, 0 = clean). */
+int tb_bleu_host(int32_t token_bytes,
+                 const void* cand_ids, int64_t cand_ld, int64_t cand_width,
+                 const int64_t* cand_len,
+                 int32_t num_refs, const void* const* ref_ids,
+                 const int64_t* ref_ld, const int64_t* ref_width,
+                 const int64_t* const* ref_len,
+                 int64_t batch, int32_t max_order,
+                 int32_t smoothing, double eps, double k, const double* weights,
+                 int64_t* num_out, int64_t* den_out,
+                 int64_t* cand_len_out, int64_t* eff_ref_out,
+                 double* scores_out, double* precisions_out, double* bp_out,
+                 int64_t* totals_out, double* corpus_out,
+                 int32_t* flags_out, void* stream);
+
 /* Replaces `apply_smoothing` + `_bp_vector` + `_geo_mean_scores`
  * (bleu.py:213-261) as used by `score_sentences_from_stats` (bleu.py:274-279).
  * With batch = 1 and pointers into a totals vector it is the corpus epilogue

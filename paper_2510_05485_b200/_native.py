@@ -60,6 +60,17 @@ SIGNATURES = {
         _P,                        # err flag
         _P, _SZ, _P,               # workspace, bytes, stream
     ]),
+    "tb_bleu_host": (ctypes.c_int, [
+        _I32,                      # token_bytes
+        _P, _I64, _I64, _P,        # cand ids, ld, width, len  (host or device)
+        _I32, _P, _P, _P, _P,      # R, ref ids[], ref ld[], ref width[], ref len[]
+        _I64, _I32,                # batch, max_order
+        _I32, _F64, _F64, _P,      # smoothing, eps, k, weights
+        _P, _P, _P, _P,            # num, den, cand_len_out, eff_ref_out   (host)
+        _P, _P, _P,                # scores, precisions, bp                 (host)
+        _P, _P,                    # totals, corpus                         (host)
+        _P, _P,                    # flags_out (host int32), stream
+    ]),
     "tb_bleu_scores": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _F64, _F64, _P,
                                       _P, _P, _P, _P]),
     "tb_bleu_totals": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _P]),
@@ -143,7 +154,14 @@ def raise_flags(flags: int, what: str = "") -> None:
         raise ValueError(f"compact ID out of range{what}")                  # _kernels.pyx:124-125
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(device: torch.device) -> int:
+    """cudaStream_t of torch's current stream on `device` (the cheap internal
+    accessor when this torch build has it)."""
+    if _raw_stream is not None:
+        return _raw_stream(device.index if device.index is not None else torch.cuda.current_device())
     return torch.cuda.current_stream(device).cuda_stream
 
 

@@ -15,7 +15,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import threading
 from dataclasses import dataclass
 from typing import Optional, Sequence, Union
 
@@ -130,21 +129,6 @@ def _weights_arg(config: BleuConfig):
     return w
 
 
-class _Pinned(threading.local):
-    buf: Optional[torch.Tensor] = None
-
-
-_pinned = _Pinned()
-
-
-def _pinned_buffer(nbytes: int) -> torch.Tensor:
-    buf = _pinned.buf
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True)
-        _pinned.buf = buf
-    return buf
-
-
 def _to_device(batch: TokenBatch, device: torch.device, want64: bool):
     """(ids, lengths, ld) on `device`; host data is copied (H2D) every call."""
     ids, lengths = batch.ids, batch.lengths
@@ -163,6 +147,81 @@ def _to_device(batch: TokenBatch, device: torch.device, want64: bool):
     return ids, lengths, ld
 
 
+def _host_view(batch: TokenBatch, want64: bool):
+    """(ids pointer, ld, width, lengths pointer, keep-alive) of a host (or
+    device) batch without copying, except int32 -> int64 widening when the
+    batches mix token types."""
+    ids, lengths = batch.ids, batch.lengths
+    if isinstance(ids, np.ndarray):
+        if want64 and ids.dtype != np.int64:
+            ids = ids.astype(np.int64)
+        ld = ids.strides[0] // ids.itemsize if ids.shape[0] > 1 else ids.shape[1]
+        ptr = ids.ctypes.data
+    else:
+        if want64 and ids.dtype != torch.int64:
+            ids = ids.to(torch.int64)
+        ld = ids.stride(0) if ids.shape[0] > 1 else ids.shape[1]
+        ptr = ids.data_ptr()
+    if isinstance(lengths, np.ndarray):
+        lptr = lengths.ctypes.data
+    else:
+        lptr = lengths.data_ptr()
+    return ptr, ld, batch.max_len, lptr, (ids, lengths)
+
+
+_INT32 = (np.dtype(np.int32), torch.int32)
+
+
+def _launch_host(candidates: TokenBatch, references: Sequence[TokenBatch], config: BleuConfig,
+                 mode: str):
+    """Host-buffer path: ONE blocking tb_bleu_host call.  Pinned token rows are
+    read by the kernel over PCIe (valid prefixes only); results land in numpy
+    arrays.  No torch ops on this path."""
+    lib = _native.load()
+    device = _native.require_cuda()
+    batches = [candidates, *references]
+    want64 = any(b.ids.dtype not in _INT32 for b in batches)
+    B, N, R = candidates.batch_size, config.max_order, len(references)
+    views = [_host_view(b, want64) for b in batches]
+    # all outputs of this mode in one allocation
+    if mode == "sentence":
+        buf = np.empty(B * (N + 2), dtype=np.float64)
+        out = {"scores": buf[:B], "bp": buf[B:2 * B], "precisions": buf[2 * B:].reshape(B, N)}
+        ptrs = (None, None, None, None, buf.ctypes.data, buf.ctypes.data + 16 * B,
+                buf.ctypes.data + 8 * B, None, None)
+    elif mode == "stats":
+        buf = np.empty(2 * B * (N + 1), dtype=np.int64)
+        out = {"num": buf[:B * N].reshape(B, N), "den": buf[B * N:2 * B * N].reshape(B, N),
+               "cand_len": buf[2 * B * N:2 * B * N + B], "eff_ref": buf[2 * B * N + B:]}
+        a = buf.ctypes.data
+        ptrs = (a, a + 8 * B * N, a + 16 * B * N, a + 16 * B * N + 8 * B, None, None, None, None, None)
+    else:
+        tot = np.empty(2 * N + 2, dtype=np.int64)
+        cor = np.empty(N + 2, dtype=np.float64)
+        out = {"totals": tot, "corpus": cor}
+        ptrs = (None,) * 7 + (tot.ctypes.data, cor.ctypes.data)
+    flags = ctypes.c_int32(0)
+    c = views[0]
+    if R == 1:
+        v = views[1]
+        ref_ids, ref_ld, ref_w, ref_lens = (ctypes.c_void_p * 1)(v[0]), (ctypes.c_int64 * 1)(v[1]), \
+            (ctypes.c_int64 * 1)(v[2]), (ctypes.c_void_p * 1)(v[3])
+    else:
+        ref_ids = (ctypes.c_void_p * R)(*[v[0] for v in views[1:]])
+        ref_ld = (ctypes.c_int64 * R)(*[v[1] for v in views[1:]])
+        ref_w = (ctypes.c_int64 * R)(*[v[2] for v in views[1:]])
+        ref_lens = (ctypes.c_void_p * R)(*[v[3] for v in views[1:]])
+    rc = lib.tb_bleu_host(
+        8 if want64 else 4, c[0], c[1], c[2], c[3], R, ref_ids, ref_ld, ref_w, ref_lens, B, N,
+        _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k, _weights_arg(config),
+        *ptrs, ctypes.byref(flags), _native.stream_handle(device))
+    if rc:
+        _native.check(rc, "tb_bleu_host")
+    if flags.value:
+        _native.raise_flags(flags.value)
+    return True, out, None
+
+
 def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: BleuConfig,
             mode: str):
     """Run tb_bleu_stats.  mode: 'stats' | 'sentence' | 'corpus'.
@@ -171,9 +230,10 @@ def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: Bl
     _check_batches(candidates, references)
     if config.max_order > _native.TB_MAX_ORDER:
         raise ValueError(f"max_order > {_native.TB_MAX_ORDER} is not supported by the device path")
+    if not candidates.is_device:
+        return _launch_host(candidates, references, config, mode)
     lib = _native.load()
-    host_mode = not candidates.is_device
-    device = (candidates.ids.device if not host_mode else _native.require_cuda())
+    device = candidates.ids.device
     _native.require_cuda(device)
     batches = [candidates, *references]
     want64 = any((b.ids.dtype != torch.int32) if isinstance(b.ids, torch.Tensor)
@@ -202,7 +262,7 @@ def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: Bl
             views[name] = out[off: off + 8 * n].view(dt)
             off += 8 * n
         err = out[:4].view(torch.int32)
-        if host_mode or mode == "corpus":
+        if mode == "corpus":
             err.zero_()  # per-sentence launches OR their flags into it (include/tensorbleu.h)
 
         ref_widths = np.array([b.max_len for b in references], dtype=np.int64)
@@ -228,28 +288,8 @@ def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: Bl
             P("totals"), P("corpus"),
             err.data_ptr(), ws.data_ptr(), ws.numel(), _native.stream_handle(device))
         _native.check(rc, "tb_bleu_stats")
-        # keep H2D sources alive until the stream is done with them
-        keep = dev
 
-    if not host_mode:
-        return False, views, None
-    # single D2H copy of [err | payload] into pinned memory, then one sync
-    pinned = _pinned_buffer(total)
-    with torch.cuda.device(device):
-        pinned[:total].copy_(out, non_blocking=True)
-        torch.cuda.current_stream(device).synchronize()
-    del keep
-    host = pinned[:total].numpy()
-    flags = int(host[:4].view(np.int32)[0])
-    if flags:
-        _native.raise_flags(flags)
-    res = {}
-    off = 8
-    for name, n, dt in sizes:
-        npdt = np.float64 if dt == torch.float64 else np.int64
-        res[name] = host[off: off + 8 * n].view(npdt).copy()
-        off += 8 * n
-    return True, res, None
+    return False, views, None
 
 
 def compute_stats(candidates: TokenBatch, references: Sequence[TokenBatch],

@@ -40,6 +40,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #define TB_VERSION_STRING "tensorbleu-b200 0.1.0 (sm_100a)"
@@ -101,6 +102,8 @@ struct StatsParams {
   double* corpus;
   unsigned long long* acc;  // kAccCopies x (2N+2), zero on entry and on exit
   unsigned int* done;       // CTA completion counter, zero on entry and on exit
+  unsigned int* arrived;    // prefix mode: groups whose rows have landed, zero on entry and on exit
+  int inflight;             // prefix mode: max groups in flight over PCIe ahead of the arrivals
   int* ws_flag;             // OR of CTA flags, zero on entry and on exit
   int32_t* err;             // written by the last CTA
   // hash table
@@ -113,6 +116,10 @@ struct StatsParams {
   // global-memory mode
   unsigned char* gtab;
   size_t gtab_stride;
+  // host-buffer mode (tb_bleu_host): stage only valid prefixes (rows come over
+  // PCIe); report flags through the completion protocol with a plain store
+  int prefix_only;
+  int err_store;
 };
 
 template <bool kSmem>
@@ -163,6 +170,84 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// --------------------------------------------------------------------------
+// Row staging shared by the shared-memory kernels.  Row s of group b is the
+// candidate (s = 0) or reference s-1; it lands at element offset
+// row_dst(s) of the token buffer.  Normally the full width is staged (widths
+// are known without reading lengths, so the copy starts at once).  In
+// prefix mode — token rows read over PCIe straight from pinned host memory
+// (tb_bleu_host) — thread 0 first reads the lengths and only the valid
+// prefixes cross the bus.
+// --------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ const T* row_src(const StatsParams& p, int s, int64_t b) {
+  return s == 0 ? static_cast<const T*>(p.cand_ids) + b * p.cand_ld
+                : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
+}
+__device__ __forceinline__ int64_t row_width(const StatsParams& p, int s) {
+  return s == 0 ? p.cand_width : p.refs[s - 1].width;
+}
+__device__ __forceinline__ int row_dst(const StatsParams& p, int s) {
+  return s == 0 ? 0 : p.cand_pad + p.ref_off[s - 1];
+}
+__device__ __forceinline__ bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+// Thread 0 only.  Prefix mode records the clamped lengths in stage_len[0..R]
+// and ORs TB_FLAG_BAD_LENGTH into *flags.
+template <typename T>
+__device__ void issue_rows(const StatsParams& p, int64_t b, int nrows, T* tok, uint64_t* mbar, int64_t* stage_len,
+                           int* flags) {
+  fence_proxy_async_smem();
+  if (p.prefix_only) {
+    for (int s = 0; s < nrows; ++s) {
+      int64_t len = s == 0 ? p.cand_len[b] : p.refs[s - 1].len[b];
+      const int64_t w = row_width(p, s);
+      if (len < 0 || len > w) {
+        *flags |= TB_FLAG_BAD_LENGTH;
+        len = len < 0 ? 0 : w;
+      }
+      stage_len[s] = len;
+    }
+  }
+  if (p.prefix_only && p.arrived && b > p.inflight) {
+    // keep at most `inflight` groups queued on the bus ahead of the arrivals, so
+    // rows land roughly in group order and counting overlaps the transfer
+    // (all lower-numbered groups are resident or done: no deadlock)
+    const unsigned int need = static_cast<unsigned int>(b - p.inflight);
+    while (true) {
+      unsigned int got;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(p.arrived) : "memory");
+      if (got >= need) break;
+      __nanosleep(128);
+    }
+  }
+  uint32_t total = 0;
+  for (int s = 0; s < nrows; ++s) {
+    const int64_t n = p.prefix_only ? stage_len[s] : row_width(p, s);
+    if (aligned16(row_src<T>(p, s, b))) total += static_cast<uint32_t>((n * sizeof(T)) & ~int64_t(15));
+  }
+  mbar_arrive_expect_tx(mbar, total);
+  for (int s = 0; s < nrows; ++s) {
+    const T* src = row_src<T>(p, s, b);
+    const int64_t n = p.prefix_only ? stage_len[s] : row_width(p, s);
+    const uint32_t bytes = static_cast<uint32_t>((n * sizeof(T)) & ~int64_t(15));
+    if (aligned16(src) && bytes > 0) bulk_g2s(tok + row_dst(p, s), src, bytes, mbar);
+  }
+}
+
+// All threads: the < 16-byte tails and rows whose address is unaligned.
+template <typename T>
+__device__ __forceinline__ void copy_row_tails(const StatsParams& p, int64_t b, int nrows, T* tok,
+                                               const int64_t* stage_len, int tid, int nthreads) {
+  for (int s = 0; s < nrows; ++s) {
+    const T* src = row_src<T>(p, s, b);
+    const int64_t n = p.prefix_only ? stage_len[s] : row_width(p, s);
+    const int64_t start = aligned16(src) ? static_cast<int64_t>(((n * sizeof(T)) & ~int64_t(15)) / sizeof(T)) : 0;
+    T* dst = tok + row_dst(p, s);
+    for (int64_t j = start + tid; j < n; j += nthreads) dst[j] = src[j];
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -357,7 +442,7 @@ __device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int&
   const int tid = threadIdx.x;
   const int N = p.max_order;
   const bool corpus = p.totals != nullptr || p.corpus != nullptr;
-  if (!corpus) {  // no cross-CTA work: report flags directly (the caller zeroed *err)
+  if (!corpus && !p.err_store) {  // no cross-CTA work: report flags directly (the caller zeroed *err)
     __syncthreads();
     if (tid == 0 && s_flags) atomicOr(p.err, s_flags);
     return;
@@ -384,6 +469,7 @@ __device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int&
     if (tid == 0) {
       *p.err = atomicExch(p.ws_flag, 0);
       *p.done = 0;
+      if (p.arrived) *p.arrived = 0;
     }
     if (p.corpus && tid < 32) {
       const int lane = tid;
@@ -762,6 +848,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int s_last, s_flags;
   __shared__ int s_nlc[2], s_nins[2];    // candidate live / inserted list lengths (by order parity)
   __shared__ int s_nlr[2][TB_MAX_REFS];  // live reference list lengths
+  __shared__ int64_t s_stage_len[TB_MAX_REFS + 1];  // prefix mode: lengths read by issue_rows
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -787,31 +874,12 @@ __global__ void __launch_bounds__(kThreads, 4)
   uint16_t* lrbase = lc + 2 * cpad;                                 // reference lists, two parities
   const uint32_t hshift = 32 - cap_log2;  // home slot = top bits of the hash
   const uint32_t bmask = (cap >> 2) - 1;  // buckets of 4 slots (one 16-byte load)
-  const T* cand_g = static_cast<const T*>(p.cand_ids);
 
-  // Stage the full rows of group b (widths are known without reading lengths):
-  // bulk copies of the 16-byte-aligned body; the < 16-byte tails and rows whose
-  // global address is unaligned are copied by the threads before the barrier.
+  // Stage the rows of group b: bulk copies of the 16-byte-aligned body (full
+  // width, or the valid prefix in prefix mode); the < 16-byte tails and rows
+  // whose global address is unaligned are copied by the threads before the barrier.
   auto issue_stage = [&](int64_t b) {
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      uint32_t total = 0;
-      for (int s = 0; s <= R; ++s) {
-        const T* src = s == 0 ? cand_g + b * p.cand_ld
-                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
-        const int64_t w = s == 0 ? p.cand_width : p.refs[s - 1].width;
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) total += static_cast<uint32_t>((w * sizeof(T)) & ~int64_t(15));
-      }
-      mbar_arrive_expect_tx(mbar, total);
-      for (int s = 0; s <= R; ++s) {
-        const T* src = s == 0 ? cand_g + b * p.cand_ld
-                              : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
-        const int64_t w = s == 0 ? p.cand_width : p.refs[s - 1].width;
-        const uint32_t bytes = static_cast<uint32_t>((w * sizeof(T)) & ~int64_t(15));
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && bytes > 0)
-          bulk_g2s(tok + (s == 0 ? 0 : cpad + p.ref_off[s - 1]), src, bytes, mbar);
-      }
-    }
+    if (tid == 0) issue_rows<T>(p, b, R + 1, tok, mbar, s_stage_len, &s_flags);
   };
 
   if (tid < 2 * N + 2) s_tot[tid] = 0;
@@ -827,7 +895,10 @@ __global__ void __launch_bounds__(kThreads, 4)
 
   for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
     // ---- lengths, per-group state (the token copy is already in flight)
-    if (tid <= R) {
+    if (p.prefix_only) {
+      __syncthreads();  // s_stage_len of this group, written by thread 0 in issue_rows
+      if (tid <= R) s_len[tid] = s_stage_len[tid];
+    } else if (tid <= R) {
       int64_t len, width;
       if (tid == 0) {
         len = p.cand_len[b];
@@ -848,17 +919,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       s_nins[tid] = 0;
     }
     if (tid < 2 * R) s_nlr[tid / R][tid % R] = 0;
-    // tails / unaligned rows
-    for (int s = 0; s <= R; ++s) {
-      const T* src = s == 0 ? cand_g + b * p.cand_ld
-                            : static_cast<const T*>(p.refs[s - 1].ids) + b * p.refs[s - 1].ld;
-      const int64_t w = s == 0 ? p.cand_width : p.refs[s - 1].width;
-      const int64_t start = ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
-                                ? static_cast<int64_t>(((w * sizeof(T)) & ~int64_t(15)) / sizeof(T))
-                                : 0;
-      T* dst = tok + (s == 0 ? 0 : cpad + p.ref_off[s - 1]);
-      for (int64_t j = start + tid; j < w; j += kThreads) dst[j] = src[j];
-    }
+    copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
     // clear the table (entries EMPTY, reference counts 0); later orders clear only used slots
     for (uint32_t s = tid; s < cap / 4; s += kThreads) reinterpret_cast<uint4*>(ent)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
     for (uint32_t s = tid; s < cap / 8; s += kThreads) {
@@ -867,6 +928,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
     mbar_wait(mbar, phase);
     phase ^= 1;
+    if (p.prefix_only && tid == 0) atomicAdd(p.arrived, 1u);
     __syncthreads();
     TB_MARK(2);
 
@@ -1190,6 +1252,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int s_last, s_flags;
   __shared__ int s_nlost, s_nsurv;
   __shared__ uint16_t s_surv[32];  // order-1 survivors when there are at most 32
+  __shared__ int64_t s_stage_len[2];  // prefix mode: lengths read by issue_rows
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -1210,24 +1273,9 @@ __global__ void __launch_bounds__(kThreads, 4)
   uint32_t* lostq = reinterpret_cast<uint32_t*>(smem + p.off_lists);  // (quad base << 4) | lost-position mask
   const uint32_t hshift = 32 - cap_log2;
   const uint32_t mask = cap - 1;
-  const T* cand_g = static_cast<const T*>(p.cand_ids);
-  const T* ref_g = static_cast<const T*>(p.refs[0].ids);
 
   auto issue_stage = [&](int64_t b) {
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      const T* srcs[2] = {cand_g + b * p.cand_ld, ref_g + b * p.refs[0].ld};
-      const int64_t ws[2] = {p.cand_width, p.refs[0].width};
-      uint32_t total = 0;
-      for (int s = 0; s < 2; ++s)
-        if ((reinterpret_cast<uintptr_t>(srcs[s]) & 15) == 0) total += static_cast<uint32_t>((ws[s] * sizeof(T)) & ~int64_t(15));
-      mbar_arrive_expect_tx(mbar, total);
-      for (int s = 0; s < 2; ++s) {
-        const uint32_t bytes = static_cast<uint32_t>((ws[s] * sizeof(T)) & ~int64_t(15));
-        if ((reinterpret_cast<uintptr_t>(srcs[s]) & 15) == 0 && bytes > 0)
-          bulk_g2s(tok + (s == 0 ? 0 : roff), srcs[s], bytes, mbar);
-      }
-    }
+    if (tid == 0) issue_rows<T>(p, b, 2, tok, mbar, s_stage_len, &s_flags);
   };
 
   if (tid < 2 * N + 2) s_tot[tid] = 0;
@@ -1241,7 +1289,10 @@ __global__ void __launch_bounds__(kThreads, 4)
   uint32_t phase = 0;
 
   for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
-    if (tid < 2) {
+    if (p.prefix_only) {
+      __syncthreads();  // s_stage_len of this group, written by thread 0 in issue_rows
+      if (tid < 2) s_len[tid] = s_stage_len[tid];
+    } else if (tid < 2) {
       const int64_t len = tid == 0 ? p.cand_len[b] : p.refs[0].len[b];
       const int64_t width = tid == 0 ? p.cand_width : p.refs[0].width;
       int64_t l = len;
@@ -1256,18 +1307,11 @@ __global__ void __launch_bounds__(kThreads, 4)
       s_nlost = 0;
       s_nsurv = 0;
     }
-    for (int s = 0; s < 2; ++s) {  // tails / unaligned rows
-      const T* src = s == 0 ? cand_g + b * p.cand_ld : ref_g + b * p.refs[0].ld;
-      const int64_t w = s == 0 ? p.cand_width : p.refs[0].width;
-      const int64_t start = ((reinterpret_cast<uintptr_t>(src) & 15) == 0)
-                                ? static_cast<int64_t>(((w * sizeof(T)) & ~int64_t(15)) / sizeof(T))
-                                : 0;
-      T* dst = tok + (s == 0 ? 0 : roff);
-      for (int64_t j = start + tid; j < w; j += kThreads) dst[j] = src[j];
-    }
+    copy_row_tails<T>(p, b, 2, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
     for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
     mbar_wait(mbar, phase);
     phase ^= 1;
+    if (p.prefix_only && tid == 0) atomicAdd(p.arrived, 1u);
     __syncthreads();
     TB_MARK(2);
 
@@ -1858,9 +1902,19 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
   }
   int64_t grid = pl.grid;
   if (persistent_fill) {
+    // occupancy per (device, dynamic smem) of this kernel instantiation, cached:
+    // the query costs microseconds on every launch otherwise
+    static thread_local struct { int dev; size_t smem; int occ; } cache[8] = {};
+    static thread_local int next = 0;
     int occ = 0;
-    TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, pl.smem_bytes));
-    if (occ < 1) occ = 1;
+    for (auto& e : cache)
+      if (e.occ > 0 && e.dev == dev && e.smem == pl.smem_bytes) occ = e.occ;
+    if (occ == 0) {
+      TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, pl.smem_bytes));
+      if (occ < 1) occ = 1;
+      cache[next] = {dev, pl.smem_bytes, occ};
+      next = (next + 1) & 7;
+    }
     const int64_t resident = static_cast<int64_t>(occ) * sms;
     grid = prm.batch < resident ? prm.batch : resident;
   }
@@ -1906,55 +1960,15 @@ int check_epi(int N, int smoothing, double eps, double k, const double* weights)
 // ==========================================================================
 // Segment kernels for the plugin surface live in plugin.cu; C ABI below.
 // ==========================================================================
-extern "C" {
-
-const char* tb_version(void) { return TB_VERSION_STRING; }
-
-const char* tb_strerror(int code) {
-  switch (code) {
-    case TB_OK: return "ok";
-    case TB_ERR_INVALID_ARG: return "invalid argument";
-    case TB_ERR_CAPACITY: return "capacity exceeded (index space overflows int64)";
-    case TB_ERR_CUDA: return "CUDA error";
-    case TB_ERR_UNSUPPORTED: return "unsupported by the device path";
-    case TB_ERR_WORKSPACE: return "workspace too small";
-    default: return "unknown error";
-  }
-}
-
-const char* tb_last_cuda_error(void) { return g_last_cuda_error; }
-
-#ifdef TB_PHASES
-int tb_debug_phase_buffer(void* buf) {
-  TB_CUDA(cudaMemcpyToSymbol(g_tb_phases, &buf, sizeof(buf)));
-  return TB_OK;
-}
-#endif
-
-size_t tb_bleu_workspace_bytes(int64_t batch, int32_t num_refs, int64_t cand_width,
-                               const int64_t* ref_widths, int32_t token_bytes, int32_t max_order) {
-  if (num_refs < 1 || num_refs > TB_MAX_REFS || max_order < 1 || max_order > TB_MAX_ORDER) return 0;
-  if (token_bytes != 4 && token_bytes != 8) return 0;
-  DevInfo* d = nullptr;
-  int smem_optin = 227 * 1024, sms = 148;
-  if (dev_info(&d) == TB_OK) {
-    smem_optin = d->smem_optin;
-    sms = d->sms;
-  }
-  Plan pl;
-  if (make_plan(batch, num_refs, cand_width, ref_widths, token_bytes, max_order, smem_optin, sms, &pl) != TB_OK)
-    return 0;
-  return pl.ws_bytes;
-}
-
-int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int64_t cand_width,
+// The launch behind tb_bleu_stats / tb_bleu_host.
+static int stats_impl(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int64_t cand_width,
                   const int64_t* cand_len, int32_t num_refs, const void* const* ref_ids,
                   const int64_t* ref_ld, const int64_t* ref_width, const int64_t* const* ref_len,
                   int64_t batch, int32_t max_order, int32_t smoothing, double eps, double k,
                   const double* weights, int64_t* num_out, int64_t* den_out, int64_t* cand_len_out,
                   int64_t* eff_ref_out, double* scores_out, double* precisions_out, double* bp_out,
                   int64_t* totals_out, double* corpus_out, int32_t* err_flag, void* workspace,
-                  size_t workspace_bytes, void* stream_) {
+                  size_t workspace_bytes, void* stream_, int prefix_only, int err_store) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (token_bytes != 4 && token_bytes != 8) return TB_ERR_INVALID_ARG;
   if (num_refs < 1) return TB_ERR_INVALID_ARG;
@@ -2014,6 +2028,7 @@ int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, in
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   prm.acc = reinterpret_cast<unsigned long long*>(ws);
   prm.done = reinterpret_cast<unsigned int*>(ws + pl.acc_bytes - 256);
+  prm.arrived = reinterpret_cast<unsigned int*>(ws + pl.acc_bytes - 256 + 8);
   prm.ws_flag = reinterpret_cast<int*>(ws + pl.acc_bytes - 256 + 4);
   prm.err = err_flag;
   prm.cap_log2 = pl.cap_log2;
@@ -2029,9 +2044,277 @@ int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, in
   prm.off_seg = pl.off_seg;
   prm.gtab = pl.smem_mode ? nullptr : ws + pl.acc_bytes;
   prm.gtab_stride = pl.gtab_stride;
+  prm.prefix_only = prefix_only && pl.smem_mode;
+  if (prm.prefix_only) {
+    // groups in flight over PCIe: ~inflight_bytes of rows (3/4 of the width on average)
+    static const int64_t inflight_bytes = [] {
+      const char* e = getenv("TB_INFLIGHT_BYTES");
+      return e ? atoll(e) : int64_t(512) << 10;
+    }();
+    int64_t per = cand_width;
+    for (int r = 0; r < num_refs; ++r) per += ref_width[r];
+    per = per * token_bytes * 3 / 4 + 1;
+    int64_t q = inflight_bytes / per;
+    prm.inflight = static_cast<int>(q < 4 ? 4 : (q > (int64_t(1) << 30) ? (int64_t(1) << 30) : q));
+  }
+  prm.err_store = err_store;
 
   if (token_bytes == 4) return launch_stats<int32_t>(prm, pl, d->sms, stream);
   return launch_stats<int64_t>(prm, pl, d->sms, stream);
+}
+
+
+// --------------------------------------------------------------------------
+// Host-buffer mode (tb_bleu_host): per-thread, per-device cached buffers.
+// --------------------------------------------------------------------------
+namespace {
+
+struct HostCtx {
+  void* ws = nullptr;            // device workspace, zero-filled (kernel contract)
+  size_t ws_bytes = 0;
+  unsigned char* pin = nullptr;  // pinned, mapped staging: lengths in, results out
+  unsigned char* pin_dev = nullptr;
+  size_t pin_bytes = 0;
+  unsigned char* dstage = nullptr;  // device staging for rows the kernel cannot read in place
+  size_t dstage_bytes = 0;
+};
+thread_local HostCtx g_host[64];
+
+int grow_device(void** buf, size_t* have, size_t want, bool zero) {
+  if (*have >= want && *buf) return TB_OK;
+  if (*buf) TB_CUDA(cudaFree(*buf));
+  *buf = nullptr;
+  *have = 0;
+  const size_t sz = want < (size_t(1) << 16) ? (size_t(1) << 16) : want + want / 4;
+  TB_CUDA(cudaMalloc(buf, sz));
+  if (zero) TB_CUDA(cudaMemset(*buf, 0, sz));
+  *have = sz;
+  return TB_OK;
+}
+
+int grow_pinned(HostCtx& c, size_t want) {
+  if (c.pin_bytes >= want && c.pin) return TB_OK;
+  if (c.pin) TB_CUDA(cudaFreeHost(c.pin));
+  c.pin = nullptr;
+  c.pin_bytes = 0;
+  const size_t sz = want < (size_t(1) << 16) ? (size_t(1) << 16) : want + want / 4;
+  void* h = nullptr;
+  TB_CUDA(cudaHostAlloc(&h, sz, cudaHostAllocMapped | cudaHostAllocPortable));
+  void* d = nullptr;
+  TB_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+  c.pin = static_cast<unsigned char*>(h);
+  c.pin_dev = static_cast<unsigned char*>(d);
+  c.pin_bytes = sz;
+  return TB_OK;
+}
+
+enum Where { kDeviceMem = 0, kPinnedHost = 1, kPageableHost = 2 };
+
+// Where does `p` live, and what address does the device use for it?
+Where classify(const void* p, const void** dev_view) {
+  *dev_view = p;
+  if (!p) return kDeviceMem;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return kPageableHost;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return kDeviceMem;
+  if (a.type == cudaMemoryTypeHost && a.devicePointer) {
+    *dev_view = a.devicePointer;
+    return kPinnedHost;
+  }
+  return kPageableHost;
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+}  // namespace
+
+extern "C" {
+
+const char* tb_version(void) { return TB_VERSION_STRING; }
+
+const char* tb_strerror(int code) {
+  switch (code) {
+    case TB_OK: return "ok";
+    case TB_ERR_INVALID_ARG: return "invalid argument";
+    case TB_ERR_CAPACITY: return "capacity exceeded (index space overflows int64)";
+    case TB_ERR_CUDA: return "CUDA error";
+    case TB_ERR_UNSUPPORTED: return "unsupported by the device path";
+    case TB_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown error";
+  }
+}
+
+const char* tb_last_cuda_error(void) { return g_last_cuda_error; }
+
+#ifdef TB_PHASES
+int tb_debug_phase_buffer(void* buf) {
+  TB_CUDA(cudaMemcpyToSymbol(g_tb_phases, &buf, sizeof(buf)));
+  return TB_OK;
+}
+#endif
+
+size_t tb_bleu_workspace_bytes(int64_t batch, int32_t num_refs, int64_t cand_width,
+                               const int64_t* ref_widths, int32_t token_bytes, int32_t max_order) {
+  if (num_refs < 1 || num_refs > TB_MAX_REFS || max_order < 1 || max_order > TB_MAX_ORDER) return 0;
+  if (token_bytes != 4 && token_bytes != 8) return 0;
+  DevInfo* d = nullptr;
+  int smem_optin = 227 * 1024, sms = 148;
+  if (dev_info(&d) == TB_OK) {
+    smem_optin = d->smem_optin;
+    sms = d->sms;
+  }
+  Plan pl;
+  if (make_plan(batch, num_refs, cand_width, ref_widths, token_bytes, max_order, smem_optin, sms, &pl) != TB_OK)
+    return 0;
+  return pl.ws_bytes;
+}
+
+int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int64_t cand_width,
+                  const int64_t* cand_len, int32_t num_refs, const void* const* ref_ids,
+                  const int64_t* ref_ld, const int64_t* ref_width, const int64_t* const* ref_len,
+                  int64_t batch, int32_t max_order, int32_t smoothing, double eps, double k,
+                  const double* weights, int64_t* num_out, int64_t* den_out, int64_t* cand_len_out,
+                  int64_t* eff_ref_out, double* scores_out, double* precisions_out, double* bp_out,
+                  int64_t* totals_out, double* corpus_out, int32_t* err_flag, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  return stats_impl(token_bytes, cand_ids, cand_ld, cand_width, cand_len, num_refs, ref_ids, ref_ld, ref_width,
+                    ref_len, batch, max_order, smoothing, eps, k, weights, num_out, den_out, cand_len_out,
+                    eff_ref_out, scores_out, precisions_out, bp_out, totals_out, corpus_out, err_flag, workspace,
+                    workspace_bytes, stream, 0, 0);
+}
+
+int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int64_t cand_width,
+                 const int64_t* cand_len, int32_t num_refs, const void* const* ref_ids,
+                 const int64_t* ref_ld, const int64_t* ref_width, const int64_t* const* ref_len,
+                 int64_t batch, int32_t max_order, int32_t smoothing, double eps, double k,
+                 const double* weights, int64_t* num_out, int64_t* den_out, int64_t* cand_len_out,
+                 int64_t* eff_ref_out, double* scores_out, double* precisions_out, double* bp_out,
+                 int64_t* totals_out, double* corpus_out, int32_t* flags_out, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (token_bytes != 4 && token_bytes != 8) return TB_ERR_INVALID_ARG;
+  if (num_refs < 1) return TB_ERR_INVALID_ARG;
+  if (num_refs > TB_MAX_REFS) return TB_ERR_UNSUPPORTED;
+  if (batch < 0 || cand_width < 0 || cand_ld < cand_width || !flags_out) return TB_ERR_INVALID_ARG;
+  if (!ref_ids || !ref_ld || !ref_width || !ref_len) return TB_ERR_INVALID_ARG;
+  int rc = check_epi(max_order, smoothing, eps, k, weights);
+  if (rc != TB_OK) return rc;
+  for (int r = 0; r < num_refs; ++r) {
+    if (ref_width[r] < 0 || ref_ld[r] < ref_width[r]) return TB_ERR_INVALID_ARG;
+    if (batch > 0 && (!ref_len[r] || (!ref_ids[r] && ref_width[r] > 0))) return TB_ERR_INVALID_ARG;
+  }
+  if (batch > 0 && ((!cand_ids && cand_width > 0) || !cand_len)) return TB_ERR_INVALID_ARG;
+  const int R = num_refs, N = max_order;
+
+  int dev = 0;
+  TB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return TB_ERR_UNSUPPORTED;
+  HostCtx& c = g_host[dev];
+  DevInfo* d = nullptr;
+  rc = dev_info(&d);
+  if (rc != TB_OK) return rc;
+  Plan pl;
+  if (batch > 0) {
+    rc = make_plan(batch, R, cand_width, ref_width, token_bytes, N, d->smem_optin, d->sms, &pl);
+    if (rc != TB_OK) return rc;
+  }
+  rc = grow_device(&c.ws, &c.ws_bytes, pl.ws_bytes > kAccBytes ? pl.ws_bytes : kAccBytes, true);
+  if (rc != TB_OK) return rc;
+
+  // ---- pinned staging layout: [err | outputs | pageable lengths]
+  const int64_t B = batch;
+  struct Out { void* user; size_t bytes; size_t off; };
+  Out outs[9] = {{num_out, size_t(B * N) * 8, 0},   {den_out, size_t(B * N) * 8, 0},
+                 {cand_len_out, size_t(B) * 8, 0},  {eff_ref_out, size_t(B) * 8, 0},
+                 {scores_out, size_t(B) * 8, 0},    {precisions_out, size_t(B * N) * 8, 0},
+                 {bp_out, size_t(B) * 8, 0},        {totals_out, size_t(2 * N + 2) * 8, 0},
+                 {corpus_out, size_t(N + 2) * 8, 0}};
+  size_t off = 256;  // err word
+  for (auto& o : outs)
+    if (o.user) {
+      o.off = off;
+      off = align_up(off + o.bytes);
+    }
+  const void* ids_in[TB_MAX_REFS + 1];
+  const int64_t* len_in[TB_MAX_REFS + 1];
+  int64_t lds[TB_MAX_REFS + 1], widths[TB_MAX_REFS + 1];
+  ids_in[0] = cand_ids;
+  len_in[0] = cand_len;
+  lds[0] = cand_ld;
+  widths[0] = cand_width;
+  for (int r = 0; r < R; ++r) {
+    ids_in[r + 1] = ref_ids[r];
+    len_in[r + 1] = ref_len[r];
+    lds[r + 1] = ref_ld[r];
+    widths[r + 1] = ref_width[r];
+  }
+  const void* ids_dev[TB_MAX_REFS + 1];
+  const int64_t* len_dev[TB_MAX_REFS + 1];
+  Where len_where[TB_MAX_REFS + 1];
+  size_t len_off[TB_MAX_REFS + 1];
+  bool need_stage[TB_MAX_REFS + 1];
+  size_t stage_off[TB_MAX_REFS + 1];
+  size_t stage_total = 0;
+  bool zero_copy = false;
+  for (int s = 0; s <= R; ++s) {
+    const void* v = nullptr;
+    len_where[s] = B > 0 ? classify(len_in[s], &v) : kDeviceMem;
+    len_dev[s] = static_cast<const int64_t*>(v);
+    len_off[s] = 0;
+    if (len_where[s] == kPageableHost) {
+      len_off[s] = off;
+      off = align_up(off + size_t(B) * 8);
+    }
+    need_stage[s] = false;
+    stage_off[s] = 0;
+    ids_dev[s] = ids_in[s];
+    if (B == 0 || widths[s] == 0) continue;
+    const void* iv = nullptr;
+    const Where w = classify(ids_in[s], &iv);
+    if (w == kDeviceMem) continue;
+    if (w == kPinnedHost && pl.smem_mode) {  // the kernel reads the valid prefixes over PCIe
+      ids_dev[s] = iv;
+      zero_copy = true;
+      continue;
+    }
+    need_stage[s] = true;
+    stage_off[s] = stage_total;
+    stage_total = align_up(stage_total + size_t((B - 1) * lds[s] + widths[s]) * token_bytes);
+  }
+  rc = grow_pinned(c, off);
+  if (rc != TB_OK) return rc;
+  if (stage_total) {
+    rc = grow_device(reinterpret_cast<void**>(&c.dstage), &c.dstage_bytes, stage_total, false);
+    if (rc != TB_OK) return rc;
+  }
+  for (int s = 0; s <= R; ++s) {
+    if (len_where[s] == kPageableHost) {
+      memcpy(c.pin + len_off[s], len_in[s], size_t(B) * 8);
+      len_dev[s] = reinterpret_cast<const int64_t*>(c.pin_dev + len_off[s]);
+    }
+    if (need_stage[s]) {
+      const size_t bytes = size_t((B - 1) * lds[s] + widths[s]) * token_bytes;
+      TB_CUDA(cudaMemcpyAsync(c.dstage + stage_off[s], ids_in[s], bytes, cudaMemcpyHostToDevice, stream));
+      ids_dev[s] = c.dstage + stage_off[s];
+    }
+  }
+  auto P = [&](int i) -> void* { return outs[i].user ? c.pin_dev + outs[i].off : nullptr; };
+  int32_t* err_host = reinterpret_cast<int32_t*>(c.pin);
+  *err_host = 0;
+  rc = stats_impl(token_bytes, ids_dev[0], cand_ld, cand_width, len_dev[0], R, ids_dev + 1, ref_ld, ref_width,
+                  len_dev + 1, B, N, smoothing, eps, k, weights, static_cast<int64_t*>(P(0)),
+                  static_cast<int64_t*>(P(1)), static_cast<int64_t*>(P(2)), static_cast<int64_t*>(P(3)),
+                  static_cast<double*>(P(4)), static_cast<double*>(P(5)), static_cast<double*>(P(6)),
+                  static_cast<int64_t*>(P(7)), static_cast<double*>(P(8)), reinterpret_cast<int32_t*>(c.pin_dev),
+                  c.ws, c.ws_bytes, stream, zero_copy ? 1 : 0, 1);
+  if (rc != TB_OK) return rc;
+  TB_CUDA(cudaStreamSynchronize(stream));
+  for (auto& o : outs)
+    if (o.user && o.bytes) memcpy(o.user, c.pin + o.off, o.bytes);
+  *flags_out = *reinterpret_cast<volatile int32_t*>(err_host);
+  return TB_OK;
 }
 
 int tb_bleu_scores(const int64_t* num, const int64_t* den, const int64_t* cand_len,
