@@ -35,6 +35,8 @@ WORKLOADS = {
     "c4": (4096, 1024, 128000, 1, "none"),
     "c5": (2048, 2048, 256000, 1, "none"),  # per-GPU shard of 16384x2048 over 8 GPUs
 }
+# c4 is corpus BLEU: one score for the whole (sharded) batch, totals NCCL-all-reduced
+MODES = {"c4": "corpus"}
 METRIC = "per-sentence BLEU-4 sentences/sec at 512x1024 tok; HBM roofline %; vs CPU ref"
 L2_FLUSH_BYTES = 256 << 20
 
@@ -129,28 +131,30 @@ def _ref_pkg():
     return oracle.reference_package()
 
 
-def cpu_reference_single(cand, refs, smoothing, repeats=3):
-    """The reference's shipped path: batchbleu.sentence_bleu, compiled backend,
-    threads=1 — 1 warm-up + `repeats` timed runs over the whole batch."""
+def cpu_reference_single(cand, refs, smoothing, repeats=3, mode="sentence"):
+    """The reference's shipped path: batchbleu.sentence_bleu (corpus_bleu in
+    corpus mode), compiled backend, threads=1 — 1 warm-up + `repeats` timed
+    runs over the whole batch."""
     bb = _ref_pkg()
     if bb is not None:
         c = bb.TokenBatch(ids=cand[0], lengths=cand[1])
         rs = [bb.TokenBatch(ids=i, lengths=l) for i, l in refs]
         cfg = bb.BleuConfig(smoothing=smoothing)
-        bb.sentence_bleu(c, rs, cfg)
+        fn = bb.corpus_bleu if mode == "corpus" else bb.sentence_bleu
+        fn(c, rs, cfg)
         ts = []
         for _ in range(repeats):
             t0 = time.perf_counter()
-            bb.sentence_bleu(c, rs, cfg)
+            fn(c, rs, cfg)
             ts.append(time.perf_counter() - t0)
-        return min(ts), "reference", "batchbleu.sentence_bleu (oracle/_ref, compiled backend, threads=1)"
+        return min(ts), "reference", f"batchbleu.{fn.__name__} (oracle/_ref, compiled backend, threads=1)"
     import oracle
     oracle.stats(cand[0][:8], cand[1][:8], [(i[:8], l[:8]) for i, l in refs])
     ts = []
     for _ in range(repeats):
         t0 = time.perf_counter()
         st = oracle.stats(cand[0], cand[1], refs)
-        oracle.scores(st, smoothing)
+        (oracle.corpus if mode == "corpus" else oracle.scores)(st, smoothing)
         ts.append(time.perf_counter() - t0)
     return min(ts), "port", "oracle/tbleu_oracle.c (C restatement, 1 thread)"
 
@@ -158,8 +162,8 @@ def cpu_reference_single(cand, refs, smoothing, repeats=3):
 _POOL_DATA = {}
 
 
-def _pool_init(cand, refs, smoothing):
-    _POOL_DATA.update(cand=cand, refs=refs, smoothing=smoothing)
+def _pool_init(cand, refs, smoothing, mode="sentence"):
+    _POOL_DATA.update(cand=cand, refs=refs, smoothing=smoothing, mode=mode)
     import oracle
     oracle.reference_package()
 
@@ -170,26 +174,42 @@ def _pool_work(span):
     cand, refs = _POOL_DATA["cand"], _POOL_DATA["refs"]
     c = bb.TokenBatch(ids=cand[0][lo:hi], lengths=cand[1][lo:hi])
     rs = [bb.TokenBatch(ids=i[lo:hi], lengths=l[lo:hi]) for i, l in refs]
-    return bb.sentence_bleu(c, rs, bb.BleuConfig(smoothing=_POOL_DATA["smoothing"])).scores
+    cfg = bb.BleuConfig(smoothing=_POOL_DATA["smoothing"])
+    if _POOL_DATA["mode"] == "corpus":
+        st = bb.compute_stats(c, rs, cfg)  # per-shard statistics; the parent aggregates
+        return st.numerators, st.denominators, st.cand_lens, st.eff_ref_lens
+    return bb.sentence_bleu(c, rs, cfg).scores
+
+
+def _pool_corpus(parts, smoothing):
+    """Corpus score of the shards' statistics, by the reference's own epilogue
+    (batchbleu.bleu.score_corpus_from_stats, bleu.py:293-305)."""
+    import batchbleu as bb
+    from batchbleu.bleu import score_corpus_from_stats
+    st = bb.SentenceStats(*[np.concatenate([p[k] for p in parts]) for k in range(4)])
+    return score_corpus_from_stats(st, bb.BleuConfig(smoothing=smoothing)).scores
 
 
 def run_reference_arm(args):
     """--impl reference: the reference's own CPU implementation on this host's
-    cores (process pool over row shards of the reference's sentence_bleu)."""
+    cores (process pool over row shards of the reference's sentence_bleu; in
+    corpus mode the shards' compute_stats, aggregated by the reference's
+    score_corpus_from_stats)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     b, l, v, r, smoothing = WORKLOADS[args.workload]
+    mode = MODES.get(args.workload, "sentence")
     cand, refs = generate_batch(b, l, v, r)
     bb = _ref_pkg()
     cores = len(os.sched_getaffinity(0))
     line = {"metric": METRIC, "unit": "sentences/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generate_batch, seed 42)",
-            "config": {"workload": f"{args.workload}: B={b} L={l} V={v} R={r} smoothing={smoothing}"}}
+            "config": {"workload": f"{args.workload}: {mode} BLEU-4, B={b} L={l} V={v} R={r} smoothing={smoothing}"}}
     if bb is None:
         # the oracle port, all cores via processes is not worth it for the C port: 1 thread
-        t, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=max(args.steps, 1))
+        t, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=max(args.steps, 1), mode=mode)
         value = b / t
         line.update(value=value, ms_per_step=t * 1e3,
                     cpu_baseline={"value": value, "unit": "sentences/s", "cores": 1, "kind": kind, "sample": what},
@@ -203,22 +223,27 @@ def run_reference_arm(args):
     spans = [(lo, min(lo + per, b)) for lo in range(0, b, per)]
     ctx = mp.get_context("fork")
     with ProcessPoolExecutor(max_workers=workers, mp_context=ctx, initializer=_pool_init,
-                             initargs=(cand, refs, smoothing)) as pool:
+                             initargs=(cand, refs, smoothing, mode)) as pool:
+        def step():
+            out = list(pool.map(_pool_work, spans))
+            if mode == "corpus":
+                _pool_corpus(out, smoothing)
         for _ in range(max(args.warmup, 1)):
-            list(pool.map(_pool_work, spans))
+            step()
         times = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            list(pool.map(_pool_work, spans))
+            step()
             times.append(time.perf_counter() - t0)
     t_pool = float(np.mean(times))
     # threads=1 shipped configuration, for the record
-    t1, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=2)
+    t1, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=2, mode=mode)
     value = b / t_pool
     line.update(value=value, ms_per_step=t_pool * 1e3,
                 cpu_baseline={"value": value, "unit": "sentences/s", "cores": workers, "kind": "reference",
-                              "sample": f"batchbleu.sentence_bleu over {len(spans)} row shards in a "
-                                        f"{workers}-process pool (harness wrapper), full {b}x{l} batch per step",
+                              "sample": f"batchbleu.{'compute_stats' if mode == 'corpus' else 'sentence_bleu'} "
+                                        f"over {len(spans)} row shards in a {workers}-process pool (harness "
+                                        f"wrapper), full {b}x{l} batch per step",
                               "single_core_value": b / t1},
                 e2e={"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
@@ -237,15 +262,26 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TB_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo, so the
+    # multi-rank logic can be exercised on a one-GPU box; never used for numbers
+    shared = os.environ.get("TB_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared else local
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+        torch.cuda.set_device(gpu)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+    dev = torch.device("cuda", gpu if world > 1 else 0)
     torch.cuda.set_device(dev)
 
     b, l, v, r, smoothing = WORKLOADS[args.workload]
+    mode = MODES.get(args.workload, "sentence")
+    corpus = mode == "corpus"
     cand_np, refs_np = generate_batch(b, l, v, r, seed=42 + rank)
     cfg = tb.BleuConfig(smoothing=smoothing)
+    mk_plan = (lambda c_, r_: tb.SentenceBleuPlan(c_, r_, cfg, stats=False, corpus=True, sentence=False)) \
+        if corpus else (lambda c_, r_: tb.SentenceBleuPlan(c_, r_, cfg))
 
     # device-resident inputs (int32 IDs).  Batch 0 is the
     # reference generator's batch; the timed loop cycles through `nbuf` distinct
@@ -258,7 +294,7 @@ def run_ours(args):
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     nbuf = max(2, -(-2 * l2_bytes // batch_bytes))
     gen = torch.Generator(device=dev)
-    plans = [tb.SentenceBleuPlan(cand, refs, cfg)]
+    plans = [mk_plan(cand, refs)]
     for k in range(1, nbuf):
         gen.manual_seed(1000 * (42 + rank) + k)
 
@@ -267,8 +303,19 @@ def run_ours(args):
             lens = torch.randint(l // 2, l + 1, (b,), generator=gen, device=dev, dtype=torch.int64)
             return tb.TokenBatch.trusted(ids, lens)
 
-        plans.append(tb.SentenceBleuPlan(draw(), [draw() for _ in range(r)], cfg))
+        plans.append(mk_plan(draw(), [draw() for _ in range(r)]))
     plan = plans[0]
+
+    def step(pl):
+        """One step: the fused kernel (graph replay); in corpus mode across
+        ranks, then the NCCL all-reduce of the 2N+2 int64 totals over NVLink
+        and the corpus epilogue on every rank."""
+        pl.replay()
+        if corpus and world > 1:
+            dist.all_reduce(pl.totals, op=dist.ReduceOp.SUM)
+            pl.corpus_from_totals()
+
+    kernels_per_step = 1 + (1 if corpus and world > 1 else 0)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -290,22 +337,22 @@ def run_ours(args):
     for pl in plans:
         pl.capture()
     for k in range(max(args.warmup, 1) * len(plans)):
-        plans[k % len(plans)].replay()
+        step(plans[k % len(plans)])
     torch.cuda.synchronize(dev)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index if world == 1 else local) as clk:
+    with ClockSampler(dev.index) as clk:
         # keep the GPU under this load for ~1 s so that nvidia-smi (>= 50 ms period)
         # samples the clocks of this workload; the timed steps follow directly
         t_until = time.perf_counter() + args.clock_window
         while time.perf_counter() < t_until:
             for k in range(200):
-                plans[k % len(plans)].replay()
+                step(plans[k % len(plans)])
             torch.cuda.synchronize(dev)
         barrier()
         torch.cuda.synchronize(dev)
         t_start.record(stream)
         for k in range(args.steps):
-            plans[k % len(plans)].replay()
+            step(plans[k % len(plans)])
         t_end.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
@@ -322,21 +369,29 @@ def run_ours(args):
     for k in range(args.steps):
         flush.zero_()
         starts[k].record(stream)
-        plan.replay()
+        step(plan)
         ends[k].record(stream)
     torch.cuda.synchronize(dev)
     step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
 
     # ---- eager public API (no graph), same device-resident inputs
+    def eager_call():
+        if not corpus:
+            return tb.sentence_bleu(cand, refs, cfg)
+        if world == 1:
+            return tb.corpus_bleu(cand, refs, cfg)
+        from paper_2510_05485_b200.distributed import allreduce_totals
+        return tb.score_corpus_from_totals(allreduce_totals(tb.corpus_totals(cand, refs, cfg)), cfg)
+
     for _ in range(2):
-        tb.sentence_bleu(cand, refs, cfg)
+        eager_call()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     eager = []
     for _ in range(args.steps):
         flush.zero_()
         e0.record(stream)
-        tb.sentence_bleu(cand, refs, cfg)
+        eager_call()
         e1.record(stream)
         e1.synchronize()
         eager.append(e0.elapsed_time(e1))
@@ -347,22 +402,33 @@ def run_ours(args):
     # tb_bleu_host: the kernel reads each pinned row's valid prefix over PCIe
     # (zero-copy) plus the lengths; results are written straight into pinned memory
     h2d = 8 * int(sum(int(ln.sum()) + ln.size for ln in [cand_np[1]] + [x for _, x in refs_np]))
-    d2h = 4 + b * (2 + cfg.max_order) * 8
+    d2h = 4 + (b * (2 + cfg.max_order) * 8 if not corpus else (3 * cfg.max_order + 4) * 8)
+
+    def e2e_call():
+        """The user's call on host buffers; results come back as numpy / floats."""
+        if not corpus:
+            return tb.sentence_bleu(hcand, hrefs, cfg)
+        if world == 1:
+            return tb.corpus_bleu(hcand, hrefs, cfg)
+        tot = torch.from_numpy(tb.corpus_totals(hcand, hrefs, cfg)).to(dev)  # this rank's shard
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)                            # NCCL, 80 B
+        return tb.score_corpus_from_totals(tot, cfg, host=True)
+
     for _ in range(2):
-        tb.sentence_bleu(hcand, hrefs, cfg)
+        e2e_call()
     barrier()
     e2e_times = []
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        res = tb.sentence_bleu(hcand, hrefs, cfg)   # returns numpy: synchronous end to end
+        res = e2e_call()   # returns numpy / float: synchronous end to end
         e2e_times.append(time.perf_counter() - t0)
     te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = b * world * args.steps / float(te.item())
-    assert res.scores.shape == (b,)
+    assert corpus or res.scores.shape == (b,)
 
     # ---- roofline of the fused kernel (the only kernel of a step)
     a_bytes = algorithmic_bytes([cand_np[1]] + [ln for _, ln in refs_np], v, b)
@@ -388,7 +454,7 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            t_cpu, kind, what = cpu_reference_single(cand_np, refs_np, smoothing, repeats=3)
+            t_cpu, kind, what = cpu_reference_single(cand_np, refs_np, smoothing, repeats=3, mode=mode)
             cpu = {"value": b / t_cpu, "unit": "sentences/s", "cores": 1, "kind": kind,
                    "sample": f"{what}; the full {b}x{l} batch, best of 3 after 1 warm-up"}
         line = {
@@ -396,11 +462,13 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (reference generate_batch: uniform IDs, lengths U[L/2, L], seed 42+rank)",
-            "config": {"workload": f"{args.workload}: per-sentence BLEU-4, B={b} L={l} V={v} R={r} "
-                                   f"smoothing={smoothing}, per GPU (weak scaling)",
+            "config": {"workload": f"{args.workload}: {'corpus' if corpus else 'per-sentence'} BLEU-4, "
+                                   f"B={b} L={l} V={v} R={r} smoothing={smoothing}, per GPU (weak scaling)",
                        "global_batch": b * world, "seq_len": l, "parallelism": f"dp{world} (row shards)",
-                       "timed_path": "SentenceBleuPlan CUDA-graph replay of tb_bleu_stats (1 kernel/step), "
-                                     "K steps back to back between two CUDA events",
+                       "timed_path": "SentenceBleuPlan CUDA-graph replay of tb_bleu_stats (1 kernel/step)"
+                                     + (", then NCCL all_reduce of the int64 totals + corpus epilogue kernel"
+                                        if corpus and world > 1 else "")
+                                     + "; K steps back to back between two CUDA events",
                        "l2": f"inputs larger than L2: steps cycle through {nbuf} distinct device-resident "
                              f"batches ({nbuf * batch_bytes / 2**20:.0f} MiB > {l2_bytes / 2**20:.0f} MiB L2); "
                              "batch 0 = reference generator seed 42, others torch.randint of the same "
@@ -413,12 +481,13 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "sentences/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "path": "sentence_bleu(TokenBatch(pinned int64 host tensors)) -> numpy: one blocking "
-                            "tb_bleu_host call; the kernel streams valid row prefixes over PCIe"},
+                    "path": f"{'corpus' if corpus else 'sentence'}_bleu(TokenBatch(pinned int64 host tensors)) "
+                            "-> numpy: one blocking tb_bleu_host call; the kernel streams valid row prefixes "
+                            "over PCIe" + (" (+ NCCL all_reduce of the totals)" if corpus and world > 1 else "")},
             "eager_api": {"value": b * world / (np.mean(eager) / 1e3), "unit": "sentences/s",
                           "ms_per_step": float(np.mean(eager)),
-                          "path": "sentence_bleu(TokenBatch(CUDA tensors)) eager, per-call allocation"},
-            "gpu_launches": args.steps * plan.kernels_per_run,
+                          "path": "public API on TokenBatch(CUDA tensors), eager, per-call allocation"},
+            "gpu_launches": args.steps * kernels_per_step,
             "clocks": clk.summary(),
             "step_flush_l2": {"value": b * world / (float(np.mean(step_ms)) / 1e3), "unit": "sentences/s",
                               "ms_per_step": float(np.mean(step_ms)), "min_ms": float(np.min(step_ms)),

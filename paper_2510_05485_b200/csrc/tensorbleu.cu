@@ -1242,6 +1242,69 @@ __device__ __forceinline__ uint32_t pair_insert_loser(uint16_t* own, uint32_t* c
   }
 }
 
+// Round-r slot of a key whose round-1 home is the top bits of h (r >= 1):
+// independent multiplicative remixes of the same 32-bit hash.
+__device__ __forceinline__ uint32_t rehash(uint32_t h, int r, uint32_t hshift) {
+  constexpr uint32_t kMul[4] = {0x85EBCA6Bu, 0xC2B2AE35u, 0x27D4EB2Fu, 0x165667B1u};
+  h ^= h >> 15;
+  return (h * kMul[r - 1]) >> hshift;
+}
+
+constexpr int kRetryRounds = 4;
+
+// Store half of retry round r for a lost position: claim slot rehash_r if it is
+// EMPTY (plain store; racing stores of the same round are resolved when verifying).
+__device__ __forceinline__ void pair_retry_store(uint16_t* own, uint32_t h, int r, uint32_t hshift, uint16_t pos) {
+  const uint32_t cs = rehash(h, r, hshift);
+  if (own[cs] == 0xffffu) own[cs] = pos;
+}
+
+// Resolve the positions on `lost` (their round-1 home slot is owned by a
+// different key).  All occurrences of a key share its home, so all of them
+// are on the list, and they move together: retry round r stores every lost
+// position into slot rehash_r(key) if that slot was EMPTY when read (plain
+// stores, one wins), a barrier, then every position verifies — the owner
+// keeps the slot, an equal key adds one to the owner's count, a different
+// key stays lost.  A key is either settled or entirely still lost after
+// each round, so the serial linear probing from the home slot that handles
+// the (rare) leftovers after kRetryRounds is self-consistent.
+// The store half of round r+1 runs in the same pass as the verify half of
+// round r: stores only ever target EMPTY slots, and every slot being verified
+// in round r is non-empty, so the two halves cannot interfere.  The caller has
+// done the store half of round 1 (in its home-slot verify pass) and a barrier.
+// `ids[pos]` receives the final slot.  All threads call it.
+template <typename HashF, typename EqF>
+__device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, uint16_t* lost, int nl, uint16_t* ids,
+                                                  uint32_t mask, uint32_t hshift, int roff, int tid, HashF hash,
+                                                  EqF eq) {
+  for (int r = 1; r <= kRetryRounds; ++r) {
+    int left = 0;
+    for (int i = tid; i < nl; i += kThreads) {
+      const uint16_t pos = lost[i];
+      if (pos == 0xffffu) continue;
+      const uint32_t h = hash(pos);
+      const uint32_t cs = rehash(h, r, hshift);
+      const uint16_t w = own[cs];
+      if (w == pos || eq(pos, w)) {
+        if (w != pos) atomicAdd(&cnt[w], pos < roff ? 1u : (1u << 16));
+        ids[pos] = static_cast<uint16_t>(cs);
+        lost[i] = 0xffffu;
+      } else {
+        left = 1;
+        if (r < kRetryRounds) pair_retry_store(own, h, r + 1, hshift, pos);
+      }
+    }
+    if (!__syncthreads_or(left)) return;
+  }
+  for (int i = tid; i < nl; i += kThreads) {
+    const uint16_t pos = lost[i];
+    if (pos == 0xffffu) continue;
+    ids[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, ids[pos], mask, pos, pos < roff ? 1u : (1u << 16),
+                                                       [&](uint16_t x) { return eq(pos, x); }));
+  }
+  __syncthreads();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 4)
     bleu_pair_kernel(const __grid_constant__ StatsParams p) {
@@ -1270,7 +1333,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot; 0xffff: n-gram unmatched
   uint16_t* own = reinterpret_cast<uint16_t*>(smem + p.off_ent);   // slot -> owner position, 0xffff = empty
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + p.off_mref);  // owner -> [ref 16 | cand 16], owner excluded
-  uint32_t* lostq = reinterpret_cast<uint32_t*>(smem + p.off_lists);  // (quad base << 4) | lost-position mask
+  uint16_t* lost = reinterpret_cast<uint16_t*>(smem + p.off_lists);  // positions whose home slot holds another key
   const uint32_t hshift = 32 - cap_log2;
   const uint32_t mask = cap - 1;
 
@@ -1368,10 +1431,13 @@ __global__ void __launch_bounds__(kThreads, 4)
       const uint32_t vm = quad(qi, p0);
       T t[4];
       load4(p0, t);
-      uint32_t home[4];
+      uint32_t hv[4], home[4];
       uint16_t w[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) home[k] = tok_hash32(t[k]) >> hshift;
+      for (int k = 0; k < 4; ++k) {
+        hv[k] = tok_hash32(t[k]);
+        home[k] = hv[k] >> hshift;
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) w[k] = own[home[k]];
       uint32_t lm = 0;
@@ -1379,32 +1445,24 @@ __global__ void __launch_bounds__(kThreads, 4)
       for (int k = 0; k < 4; ++k) {
         const int pos = p0 + k;
         if ((vm >> k & 1u) && w[k] != pos) {
-          if (tok[w[k]] == t[k])
+          if (tok[w[k]] == t[k]) {
             atomicAdd(&cnt[w[k]], inc_of(pos));
-          else
+          } else {
             lm |= 1u << k;
+            pair_retry_store(own, hv[k], 1, hshift, static_cast<uint16_t>(pos));
+          }
         }
       }
       *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
-      if (lm) lostq[atomicAdd(&s_nlost, 1)] = (static_cast<uint32_t>(p0) << 4) | lm;
+      for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
     }
     __syncthreads();
     TB_MARK(29);
-    if (s_nlost) {  // deferred inserts of positions whose home slot holds another token
-      const int nl = s_nlost;
-      for (int i = tid; i < nl; i += kThreads) {
-        const uint32_t e = lostq[i];
-        const int p0 = static_cast<int>(e >> 4);
-        for (int k = 0; k < 4; ++k) {
-          if (!(e >> k & 1u)) continue;
-          const int pos = p0 + k;
-          const T t = tok[pos];
-          id1[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, id1[pos], mask, static_cast<uint16_t>(pos),
-                                                             inc_of(pos), [&](uint16_t x) { return tok[x] == t; }));
-        }
-      }
-      __syncthreads();
-    }
+    TB_NOTE(27, s_nlost);
+    if (s_nlost)  // positions whose home slot holds another token
+      pair_resolve_lost(own, cnt, lost, s_nlost, id1, mask, hshift, roff, tid,
+                        [&](uint16_t q) { return tok_hash32(tok[q]); },
+                        [&](uint16_t a, uint16_t b) { return tok[a] == tok[b]; });
     TB_MARK(3);
     {  // liveness + clipped count (added once per slot by its owner)
       unsigned int hits = 0;
@@ -1530,34 +1588,26 @@ __global__ void __launch_bounds__(kThreads, 4)
           for (int k = 0; k < 4; ++k) {
             if (key[k] == ~0u) continue;
             const int pos = p0 + k;
-            const uint32_t home = (key[k] * 0x9E3779B1u) >> hshift;
+            const uint32_t hk = key[k] * 0x9E3779B1u;
+            const uint32_t home = hk >> hshift;
             const uint16_t w = own[home];
             if (w != pos) {
-              if (kc[w] == key[k])
+              if (kc[w] == key[k]) {
                 atomicAdd(&cnt[w], inc_of(pos));
-              else
+              } else {
                 lm |= 1u << k;
+                pair_retry_store(own, hk, 1, hshift, static_cast<uint16_t>(pos));
+              }
             }
             idn[pos] = static_cast<uint16_t>(home);
           }
-          if (lm) lostq[atomicAdd(&s_nlost, 1)] = (static_cast<uint32_t>(p0) << 4) | lm;
+          for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
         }
         __syncthreads();
-        if (s_nlost) {
-          const int nl = s_nlost;
-          for (int i = tid; i < nl; i += kThreads) {
-            const uint32_t e = lostq[i];
-            const int p0 = static_cast<int>(e >> 4);
-            for (int k = 0; k < 4; ++k) {
-              if (!(e >> k & 1u)) continue;
-              const int pos = p0 + k;
-              const uint32_t key = kc[pos];
-              idn[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, idn[pos], mask, static_cast<uint16_t>(pos),
-                                                                 inc_of(pos), [&](uint16_t x) { return kc[x] == key; }));
-            }
-          }
-          __syncthreads();
-        }
+        if (s_nlost)
+          pair_resolve_lost(own, cnt, lost, s_nlost, idn, mask, hshift, roff, tid,
+                            [&](uint16_t q) { return kc[q] * 0x9E3779B1u; },
+                            [&](uint16_t a, uint16_t b) { return kc[a] == kc[b]; });
         unsigned int hits = 0;
         bool live_c = false;
         for (int qi = tid; qi < nq; qi += kThreads) {
@@ -1789,8 +1839,8 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       o = round_up(o + c * 2, 16);
       offs[3] = o;                       // cnt (u32 per position)
       o = round_up(o + ptot * 4, 16);
-      offs[4] = o;                       // lost-quad list (u32 per quad)
-      o = round_up(o + (ptot / 4) * 4, 16);
+      offs[4] = o;                       // lost-position list (u16 per position)
+      o = round_up(o + ptot * 2, 16);
       offs[5] = o;
       return o;
     };

@@ -55,12 +55,32 @@ def _world(group) -> tuple[int, int]:
     return dist.get_rank(group), dist.get_world_size(group)
 
 
+def _host_staged(group) -> bool:
+    """Backends without CUDA-tensor collectives (gloo: CPU tensors only for
+    some ops) get host-staged copies; NCCL works on device memory directly."""
+    return dist.get_backend(group) != "nccl"
+
+
 def allreduce_totals(totals: torch.Tensor, group=None) -> torch.Tensor:
     """SUM-all-reduce of the int64 corpus totals (in place, returned)."""
     rank, world = _world(group)
     if world > 1:
-        dist.all_reduce(totals, op=dist.ReduceOp.SUM, group=group)
+        if totals.is_cuda and _host_staged(group):
+            host = totals.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+            totals.copy_(host)
+        else:
+            dist.all_reduce(totals, op=dist.ReduceOp.SUM, group=group)
     return totals
+
+
+def _all_gather(out: torch.Tensor, buf: torch.Tensor, group) -> None:
+    if buf.is_cuda and _host_staged(group):
+        host = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(host, buf.cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, buf, group=group)
 
 
 def sharded_sentence_bleu(candidates: TokenBatch, references: Sequence[TokenBatch],
@@ -81,7 +101,7 @@ def sharded_sentence_bleu(candidates: TokenBatch, references: Sequence[TokenBatc
     buf = torch.zeros(per, dtype=torch.float64, device=dev)
     buf[: hi - lo] = res.scores
     out = torch.empty(per * world, dtype=torch.float64, device=dev)
-    dist.all_gather_into_tensor(out, buf, group=group)
+    _all_gather(out, buf, group)
     return BleuResult(scores=out[: candidates.batch_size], precisions=res.precisions,
                       brevity_penalty=res.brevity_penalty)
 

@@ -32,7 +32,8 @@ class SentenceBleuPlan:
     kernels_per_run = 1
 
     def __init__(self, candidates: TokenBatch, references: Sequence[TokenBatch],
-                 config: Optional[BleuConfig] = None, *, stats: bool = True, corpus: bool = False):
+                 config: Optional[BleuConfig] = None, *, stats: bool = True, corpus: bool = False,
+                 sentence: bool = True):
         config = config or BleuConfig()
         _check_batches(candidates, references)
         if not candidates.is_device or not all(r.is_device for r in references):
@@ -50,9 +51,9 @@ class SentenceBleuPlan:
         self.batch_size, self.max_order = B, N
         tb = candidates.ids.element_size()
         with torch.cuda.device(dev):
-            self.scores = torch.empty(B, dtype=torch.float64, device=dev)
-            self.precisions = torch.empty((B, N), dtype=torch.float64, device=dev)
-            self.brevity_penalty = torch.empty(B, dtype=torch.float64, device=dev)
+            self.scores = torch.empty(B, dtype=torch.float64, device=dev) if sentence else None
+            self.precisions = torch.empty((B, N), dtype=torch.float64, device=dev) if sentence else None
+            self.brevity_penalty = torch.empty(B, dtype=torch.float64, device=dev) if sentence else None
             self.numerators = torch.empty((B, N), dtype=torch.int64, device=dev) if stats else None
             self.denominators = torch.empty((B, N), dtype=torch.int64, device=dev) if stats else None
             self.cand_lens = torch.empty(B, dtype=torch.int64, device=dev) if stats else None
@@ -84,6 +85,22 @@ class SentenceBleuPlan:
             p(self.workspace), self.workspace.numel())
         self._fn = lib.tb_bleu_stats
         self.graph: Optional[torch.cuda.CUDAGraph] = None
+
+    def corpus_from_totals(self) -> None:
+        """Corpus epilogue (score, BP, precisions -> self.corpus) of the int64
+        totals in self.totals — after they were all-reduced across ranks
+        (score_corpus_from_stats, bleu.py:301-305).  One tiny launch."""
+        if self.totals is None:
+            raise ValueError("plan was built without corpus=True")
+        lib = _native.load()
+        N = self.max_order
+        t0, c0 = self.totals.data_ptr(), self.corpus.data_ptr()
+        rc = lib.tb_bleu_scores(t0, t0 + 8 * N, t0 + 16 * N, t0 + 16 * N + 8, 1, N,
+                                _native.SMOOTHING_CODES[self.config.smoothing], self.config.eps,
+                                self.config.k, _weights_arg(self.config), c0, c0 + 16, c0 + 8,
+                                _native.stream_handle(self.device))
+        if rc:
+            _native.check(rc, "tb_bleu_scores")
 
     def run(self) -> None:
         """Launch on the current stream (asynchronous)."""
