@@ -112,6 +112,23 @@ def load():
     return _lib
 
 
+_hp = None
+
+
+def hostpath():
+    """The CPython binding of tb_bleu_host (built in-tree next to the library)."""
+    global _hp
+    if _hp is None:
+        load()
+        try:
+            from . import _hostpath
+        except ImportError as e:
+            raise NativeLibraryError(f"the _hostpath extension is not built ({e}); run "
+                                     "`python -c 'import __graft_entry__ as g; g.build()'`") from e
+        _hp = _hostpath
+    return _hp
+
+
 def require_cuda(device: Optional[torch.device] = None) -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2510_05485_b200 needs a CUDA device (B200, sm_100a); "

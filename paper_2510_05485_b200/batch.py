@@ -112,6 +112,31 @@ class TokenBatch:
         obj._init_device(validate=False)
         return obj
 
+    def _row_view(self, want64: bool):
+        """(ids pointer, ld, width, lengths pointer, token bytes) of this batch
+        for the C ABI, plus the arrays that keep those pointers alive.  Cached
+        (the batch is immutable); int32 IDs are widened once when `want64`
+        (batches of one call must share a token width)."""
+        key = "_view64" if want64 else "_view"
+        v = self.__dict__.get(key)
+        if v is not None:
+            return v
+        ids, lengths = self.ids, self.lengths
+        if isinstance(ids, np.ndarray):
+            if want64 and ids.dtype != np.int64:
+                ids = ids.astype(np.int64)
+            ptr, isz, ld = ids.ctypes.data, ids.itemsize, ids.strides[0] // ids.itemsize
+        else:
+            if want64 and ids.dtype != torch.int64:
+                ids = ids.to(torch.int64)
+            ptr, isz, ld = ids.data_ptr(), ids.element_size(), ids.stride(0)
+        if ids.shape[0] <= 1:
+            ld = ids.shape[1]
+        lptr = lengths.ctypes.data if isinstance(lengths, np.ndarray) else lengths.data_ptr()
+        v = ((ptr, ld, int(ids.shape[1]), lptr, isz), (ids, lengths))
+        object.__setattr__(self, key, v)
+        return v
+
     @property
     def batch_size(self) -> int:
         return int(self.ids.shape[0])

@@ -129,6 +129,10 @@ def _weights_arg(config: BleuConfig):
     return w
 
 
+def _weights_addr(config: BleuConfig) -> int:
+    return ctypes.addressof(_weights_arg(config))
+
+
 def _to_device(batch: TokenBatch, device: torch.device, want64: bool):
     """(ids, lengths, ld) on `device`; host data is copied (H2D) every call."""
     ids, lengths = batch.ids, batch.lengths
@@ -147,79 +151,82 @@ def _to_device(batch: TokenBatch, device: torch.device, want64: bool):
     return ids, lengths, ld
 
 
-def _host_view(batch: TokenBatch, want64: bool):
-    """(ids pointer, ld, width, lengths pointer, keep-alive) of a host (or
-    device) batch without copying, except int32 -> int64 widening when the
-    batches mix token types."""
-    ids, lengths = batch.ids, batch.lengths
-    if isinstance(ids, np.ndarray):
-        if want64 and ids.dtype != np.int64:
-            ids = ids.astype(np.int64)
-        ld = ids.strides[0] // ids.itemsize if ids.shape[0] > 1 else ids.shape[1]
-        ptr = ids.ctypes.data
-    else:
-        if want64 and ids.dtype != torch.int64:
-            ids = ids.to(torch.int64)
-        ld = ids.stride(0) if ids.shape[0] > 1 else ids.shape[1]
-        ptr = ids.data_ptr()
-    if isinstance(lengths, np.ndarray):
-        lptr = lengths.ctypes.data
-    else:
-        lptr = lengths.data_ptr()
-    return ptr, ld, batch.max_len, lptr, (ids, lengths)
-
-
 _INT32 = (np.dtype(np.int32), torch.int32)
+_MODES = {"stats": 0, "sentence": 1, "corpus": 2}
+_OUT_NAMES = {"stats": ("num", "den", "cand_len", "eff_ref"),
+              "sentence": ("scores", "precisions", "bp"),
+              "corpus": ("totals", "corpus")}
 
 
 def _launch_host(candidates: TokenBatch, references: Sequence[TokenBatch], config: BleuConfig,
                  mode: str):
-    """Host-buffer path: ONE blocking tb_bleu_host call.  Pinned token rows are
-    read by the kernel over PCIe (valid prefixes only); results land in numpy
-    arrays.  No torch ops on this path."""
-    lib = _native.load()
+    """Host-buffer path: ONE blocking tb_bleu_host call through the native
+    binding (_hostpath, GIL released).  Pinned token rows are read by the
+    kernel over PCIe (valid prefixes only); results come back as numpy."""
+    hp = _native.hostpath()
     device = _native.require_cuda()
-    batches = [candidates, *references]
+    batches = (candidates, *references)
     want64 = any(b.ids.dtype not in _INT32 for b in batches)
-    B, N, R = candidates.batch_size, config.max_order, len(references)
-    views = [_host_view(b, want64) for b in batches]
-    # all outputs of this mode in one allocation
-    if mode == "sentence":
-        buf = np.empty(B * (N + 2), dtype=np.float64)
-        out = {"scores": buf[:B], "bp": buf[B:2 * B], "precisions": buf[2 * B:].reshape(B, N)}
-        ptrs = (None, None, None, None, buf.ctypes.data, buf.ctypes.data + 16 * B,
-                buf.ctypes.data + 8 * B, None, None)
-    elif mode == "stats":
-        buf = np.empty(2 * B * (N + 1), dtype=np.int64)
-        out = {"num": buf[:B * N].reshape(B, N), "den": buf[B * N:2 * B * N].reshape(B, N),
-               "cand_len": buf[2 * B * N:2 * B * N + B], "eff_ref": buf[2 * B * N + B:]}
-        a = buf.ctypes.data
-        ptrs = (a, a + 8 * B * N, a + 16 * B * N, a + 16 * B * N + 8 * B, None, None, None, None, None)
-    else:
-        tot = np.empty(2 * N + 2, dtype=np.int64)
-        cor = np.empty(N + 2, dtype=np.float64)
-        out = {"totals": tot, "corpus": cor}
-        ptrs = (None,) * 7 + (tot.ctypes.data, cor.ctypes.data)
-    flags = ctypes.c_int32(0)
-    c = views[0]
-    if R == 1:
-        v = views[1]
-        ref_ids, ref_ld, ref_w, ref_lens = (ctypes.c_void_p * 1)(v[0]), (ctypes.c_int64 * 1)(v[1]), \
-            (ctypes.c_int64 * 1)(v[2]), (ctypes.c_void_p * 1)(v[3])
-    else:
-        ref_ids = (ctypes.c_void_p * R)(*[v[0] for v in views[1:]])
-        ref_ld = (ctypes.c_int64 * R)(*[v[1] for v in views[1:]])
-        ref_w = (ctypes.c_int64 * R)(*[v[2] for v in views[1:]])
-        ref_lens = (ctypes.c_void_p * R)(*[v[3] for v in views[1:]])
-    rc = lib.tb_bleu_host(
-        8 if want64 else 4, c[0], c[1], c[2], c[3], R, ref_ids, ref_ld, ref_w, ref_lens, B, N,
-        _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k, _weights_arg(config),
-        *ptrs, ctypes.byref(flags), _native.stream_handle(device))
+    views = tuple(b._row_view(want64)[0] for b in batches)
+    rc, flags, *outs = hp.run(_MODES[mode], views, candidates.batch_size, config.max_order,
+                              _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k,
+                              _weights_addr(config), _native.stream_handle(device))
     if rc:
         _native.check(rc, "tb_bleu_host")
-    if flags.value:
-        _native.raise_flags(flags.value)
-    return True, out, None
+    if flags:
+        _native.raise_flags(flags)
+    return True, dict(zip(_OUT_NAMES[mode], outs)), None
+
+
+_ws_bytes_cache: dict = {}
+_err_words: dict = {}
+
+
+def _launch_device(candidates: TokenBatch, references: Sequence[TokenBatch], config: BleuConfig,
+                   mode: str, device: torch.device):
+    """All rows already on `device`: one asynchronous tb_bleu_stats launch
+    through the native binding, outputs carved from one allocation, no host
+    synchronisation."""
+    hp = _native.hostpath()
+    batches = (candidates, *references)
+    want64 = any(b.ids.dtype != torch.int32 for b in batches)
+    views = tuple(b._row_view(want64)[0] for b in batches)
+    B, N = candidates.batch_size, config.max_order
+    key = (device.index, B, tuple(v[2] for v in views), views[0][4], N)
+    wsb = _ws_bytes_cache.get(key)
+    if wsb is None:
+        widths = np.array([v[2] for v in views[1:]], dtype=np.int64)
+        wsb = _native.load().tb_bleu_workspace_bytes(B, len(references), views[0][2], widths.ctypes.data,
+                                                     views[0][4], N)
+        if wsb == 0:
+            raise ValueError("unsupported shape for the device path")
+        _ws_bytes_cache[key] = wsb
+    ws = _native.workspace.get(device, wsb)
+    err = _err_words.get(device.index)
+    if err is None:
+        err = _err_words[device.index] = torch.zeros(1, dtype=torch.int32, device=device)
+    if mode == "sentence":
+        buf = torch.empty(B * (N + 2), dtype=torch.float64, device=device)
+        a = buf.data_ptr()
+        outs = (None, None, None, None, a, a + 16 * B, a + 8 * B, None, None)
+        views_out = {"scores": buf[:B], "bp": buf[B:2 * B], "precisions": buf[2 * B:].view(B, N)}
+    elif mode == "stats":
+        buf = torch.empty(2 * B * (N + 1), dtype=torch.int64, device=device)
+        a = buf.data_ptr()
+        outs = (a, a + 8 * B * N, a + 16 * B * N, a + 16 * B * N + 8 * B, None, None, None, None, None)
+        views_out = {"num": buf[:B * N], "den": buf[B * N:2 * B * N], "cand_len": buf[2 * B * N:2 * B * N + B],
+                     "eff_ref": buf[2 * B * N + B:]}
+    else:
+        buf = torch.empty(3 * N + 4, dtype=torch.int64, device=device)
+        a = buf.data_ptr()
+        outs = (None,) * 7 + (a, a + 8 * (2 * N + 2))
+        views_out = {"totals": buf[:2 * N + 2], "corpus": buf[2 * N + 2:].view(torch.float64)}
+    rc = hp.launch(views, B, N, _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k,
+                   _weights_addr(config), outs, err.data_ptr(), ws.data_ptr(), ws.numel(),
+                   _native.stream_handle(device))
+    if rc:
+        _native.check(rc, "tb_bleu_stats")
+    return False, views_out, None
 
 
 def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: BleuConfig,
@@ -232,6 +239,9 @@ def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: Bl
         raise ValueError(f"max_order > {_native.TB_MAX_ORDER} is not supported by the device path")
     if not candidates.is_device:
         return _launch_host(candidates, references, config, mode)
+    device = candidates.ids.device
+    if all(r.is_device and r.ids.device == device for r in references):
+        return _launch_device(candidates, references, config, mode, device)
     lib = _native.load()
     device = candidates.ids.device
     _native.require_cuda(device)

@@ -34,9 +34,9 @@ def main():
     dev = torch.device("cuda", 0)
     print("require_cuda          ", t(lambda: _native.require_cuda()))
     print("stream_handle         ", t(lambda: _native.stream_handle(dev)))
-    print("host_view x2          ", t(lambda: [bleu._host_view(b, True) for b in (cand, refs[0])]))
+    print("row views x2 (cached) ", t(lambda: [b._row_view(True) for b in (cand, refs[0])]))
     print("sentence_bleu (tiny)  ", t(lambda: tb.sentence_bleu(cand, refs, cfg)))
-    v = bleu._host_view(cand, True)
+    v = cand._row_view(True)[0]
     out = np.empty(1)
     flags = ctypes.c_int32(0)
     w = bleu._weights_arg(cfg)
