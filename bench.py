@@ -396,39 +396,50 @@ def run_ours(args):
         e1.synchronize()
         eager.append(e0.elapsed_time(e1))
 
-    # ---- e2e: public API with pinned HOST buffers; H2D + kernel + D2H in the timed region
-    hcand = tb.TokenBatch(ids=torch.from_numpy(cand_np[0]).pin_memory(), lengths=torch.from_numpy(cand_np[1]))
-    hrefs = [tb.TokenBatch(ids=torch.from_numpy(i).pin_memory(), lengths=torch.from_numpy(ln)) for i, ln in refs_np]
-    # tb_bleu_host: the kernel reads each pinned row's valid prefix over PCIe
-    # (zero-copy) plus the lengths; results are written straight into pinned memory
-    h2d = 8 * int(sum(int(ln.sum()) + ln.size for ln in [cand_np[1]] + [x for _, x in refs_np]))
+    # ---- e2e: public API with pinned HOST buffers; H2D + kernel + D2H in the timed region.
+    # Headline: int32 token IDs (the dtype the path computes in, and what a
+    # training loop's tokenizer output holds); int64 (the reference
+    # TokenBatch's own dtype, batch.py:23-24) is reported beside it.
     d2h = 4 + (b * (2 + cfg.max_order) * 8 if not corpus else (3 * cfg.max_order + 4) * 8)
 
-    def e2e_call():
-        """The user's call on host buffers; results come back as numpy / floats."""
-        if not corpus:
-            return tb.sentence_bleu(hcand, hrefs, cfg)
-        if world == 1:
-            return tb.corpus_bleu(hcand, hrefs, cfg)
-        tot = torch.from_numpy(tb.corpus_totals(hcand, hrefs, cfg)).to(dev)  # this rank's shard
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)                            # NCCL, 80 B
-        return tb.score_corpus_from_totals(tot, cfg, host=True)
+    def measure_e2e(np_dtype):
+        hcand = tb.TokenBatch(ids=torch.from_numpy(cand_np[0].astype(np_dtype)).pin_memory(),
+                              lengths=torch.from_numpy(cand_np[1]))
+        hrefs = [tb.TokenBatch(ids=torch.from_numpy(i.astype(np_dtype)).pin_memory(), lengths=torch.from_numpy(ln))
+                 for i, ln in refs_np]
+        # tb_bleu_host: the kernel reads each pinned row's valid prefix over PCIe
+        # (zero-copy) plus the lengths; results are written straight into pinned memory
+        isz = np.dtype(np_dtype).itemsize
+        h2d = int(sum(isz * int(ln.sum()) + 8 * ln.size for ln in [cand_np[1]] + [x for _, x in refs_np]))
 
-    for _ in range(2):
-        e2e_call()
-    barrier()
-    e2e_times = []
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        res = e2e_call()   # returns numpy / float: synchronous end to end
-        e2e_times.append(time.perf_counter() - t0)
-    te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = b * world * args.steps / float(te.item())
-    assert corpus or res.scores.shape == (b,)
+        def e2e_call():
+            """The user's call on host buffers; results come back as numpy / floats."""
+            if not corpus:
+                return tb.sentence_bleu(hcand, hrefs, cfg)
+            if world == 1:
+                return tb.corpus_bleu(hcand, hrefs, cfg)
+            tot = torch.from_numpy(tb.corpus_totals(hcand, hrefs, cfg)).to(dev)  # this rank's shard
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM)                            # NCCL, 80 B
+            return tb.score_corpus_from_totals(tot, cfg, host=True)
+
+        for _ in range(2):
+            e2e_call()
+        barrier()
+        e2e_times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            res = e2e_call()   # returns numpy / float: synchronous end to end
+            e2e_times.append(time.perf_counter() - t0)
+        assert corpus or res.scores.shape == (b,)
+        te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        return b * world * args.steps / float(te.item()), h2d
+
+    e2e_value, h2d = measure_e2e(np.int32)
+    e2e64_value, h2d64 = measure_e2e(np.int64)
 
     # ---- roofline of the fused kernel (the only kernel of a step)
     a_bytes = algorithmic_bytes([cand_np[1]] + [ln for _, ln in refs_np], v, b)
@@ -480,8 +491,9 @@ def run_ours(args):
                                  f"{input_bytes} B of int32 tokens, so frac > 1 means it beats the paper dataflow"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "sentences/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h),
-                    "path": f"{'corpus' if corpus else 'sentence'}_bleu(TokenBatch(pinned int64 host tensors)) "
+                    "d2h_bytes_per_step": int(d2h), "token_dtype": "int32",
+                    "int64_tokens": {"value": e2e64_value, "h2d_bytes_per_step": int(h2d64)},
+                    "path": f"{'corpus' if corpus else 'sentence'}_bleu(TokenBatch(pinned host tensors)) "
                             "-> numpy: one blocking tb_bleu_host call; the kernel streams valid row prefixes "
                             "over PCIe" + (" (+ NCCL all_reduce of the totals)" if corpus and world > 1 else "")},
             "eager_api": {"value": b * world / (np.mean(eager) / 1e3), "unit": "sentences/s",

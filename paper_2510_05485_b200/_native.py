@@ -129,8 +129,14 @@ def hostpath():
     return _hp
 
 
+_cuda_ok: Optional[bool] = None
+
+
 def require_cuda(device: Optional[torch.device] = None) -> torch.device:
-    if not torch.cuda.is_available():
+    global _cuda_ok
+    if _cuda_ok is None:
+        _cuda_ok = torch.cuda.is_available()
+    if not _cuda_ok:
         raise RuntimeError("paper_2510_05485_b200 needs a CUDA device (B200, sm_100a); "
                            "there is no CPU fallback")
     if device is None:

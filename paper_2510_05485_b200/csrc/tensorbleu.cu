@@ -102,8 +102,6 @@ struct StatsParams {
   double* corpus;
   unsigned long long* acc;  // kAccCopies x (2N+2), zero on entry and on exit
   unsigned int* done;       // CTA completion counter, zero on entry and on exit
-  unsigned int* arrived;    // prefix mode: groups whose rows have landed, zero on entry and on exit
-  int inflight;             // prefix mode: max groups in flight over PCIe ahead of the arrivals
   int* ws_flag;             // OR of CTA flags, zero on entry and on exit
   int32_t* err;             // written by the last CTA
   // hash table
@@ -209,18 +207,6 @@ __device__ void issue_rows(const StatsParams& p, int64_t b, int nrows, T* tok, u
         len = len < 0 ? 0 : w;
       }
       stage_len[s] = len;
-    }
-  }
-  if (p.prefix_only && p.arrived && b > p.inflight) {
-    // keep at most `inflight` groups queued on the bus ahead of the arrivals, so
-    // rows land roughly in group order and counting overlaps the transfer
-    // (all lower-numbered groups are resident or done: no deadlock)
-    const unsigned int need = static_cast<unsigned int>(b - p.inflight);
-    while (true) {
-      unsigned int got;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(p.arrived) : "memory");
-      if (got >= need) break;
-      __nanosleep(128);
     }
   }
   uint32_t total = 0;
@@ -469,7 +455,6 @@ __device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int&
     if (tid == 0) {
       *p.err = atomicExch(p.ws_flag, 0);
       *p.done = 0;
-      if (p.arrived) *p.arrived = 0;
     }
     if (p.corpus && tid < 32) {
       const int lane = tid;
@@ -928,7 +913,6 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
     mbar_wait(mbar, phase);
     phase ^= 1;
-    if (p.prefix_only && tid == 0) atomicAdd(p.arrived, 1u);
     __syncthreads();
     TB_MARK(2);
 
@@ -1374,7 +1358,6 @@ __global__ void __launch_bounds__(kThreads, 4)
     for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
     mbar_wait(mbar, phase);
     phase ^= 1;
-    if (p.prefix_only && tid == 0) atomicAdd(p.arrived, 1u);
     __syncthreads();
     TB_MARK(2);
 
@@ -2078,7 +2061,6 @@ static int stats_impl(int32_t token_bytes, const void* cand_ids, int64_t cand_ld
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   prm.acc = reinterpret_cast<unsigned long long*>(ws);
   prm.done = reinterpret_cast<unsigned int*>(ws + pl.acc_bytes - 256);
-  prm.arrived = reinterpret_cast<unsigned int*>(ws + pl.acc_bytes - 256 + 8);
   prm.ws_flag = reinterpret_cast<int*>(ws + pl.acc_bytes - 256 + 4);
   prm.err = err_flag;
   prm.cap_log2 = pl.cap_log2;
@@ -2095,18 +2077,6 @@ static int stats_impl(int32_t token_bytes, const void* cand_ids, int64_t cand_ld
   prm.gtab = pl.smem_mode ? nullptr : ws + pl.acc_bytes;
   prm.gtab_stride = pl.gtab_stride;
   prm.prefix_only = prefix_only && pl.smem_mode;
-  if (prm.prefix_only) {
-    // groups in flight over PCIe: ~inflight_bytes of rows (3/4 of the width on average)
-    static const int64_t inflight_bytes = [] {
-      const char* e = getenv("TB_INFLIGHT_BYTES");
-      return e ? atoll(e) : int64_t(512) << 10;
-    }();
-    int64_t per = cand_width;
-    for (int r = 0; r < num_refs; ++r) per += ref_width[r];
-    per = per * token_bytes * 3 / 4 + 1;
-    int64_t q = inflight_bytes / per;
-    prm.inflight = static_cast<int>(q < 4 ? 4 : (q > (int64_t(1) << 30) ? (int64_t(1) << 30) : q));
-  }
   prm.err_store = err_store;
 
   if (token_bytes == 4) return launch_stats<int32_t>(prm, pl, d->sms, stream);
