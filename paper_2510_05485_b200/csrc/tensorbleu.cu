@@ -1289,6 +1289,37 @@ __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, 
   __syncthreads();
 }
 
+// Slot of token t among the inserted (candidate) tokens, or -1; *owner gets its
+// owner position.  Follows an inserted key's placement order: home slot, the
+// retry rounds' slots, then linear probing from home + 1 — a key sits at the
+// first slot of that chain that it owns, and every earlier slot of the chain is
+// owned by another key (slots never empty again), so an EMPTY slot ends the search.
+// pair_find_retry continues after a home slot owned by a different token.
+template <typename T>
+__device__ __forceinline__ int pair_find_retry(const uint16_t* own, const T* tok, T t, uint32_t h, uint32_t hshift,
+                                            uint32_t mask, uint16_t* owner) {
+  const uint32_t home = h >> hshift;
+  uint16_t o;
+#pragma unroll 1
+  for (int r = 1; r <= kRetryRounds; ++r) {
+    const uint32_t cs = rehash(h, r, hshift);
+    o = own[cs];
+    if (o == 0xffffu) return -1;
+    if (tok[o] == t) {
+      *owner = o;
+      return static_cast<int>(cs);
+    }
+  }
+  for (uint32_t s = (home + 1) & mask;; s = (s + 1) & mask) {
+    o = own[s];
+    if (o == 0xffffu) return -1;
+    if (tok[o] == t) {
+      *owner = o;
+      return static_cast<int>(s);
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 4)
     bleu_pair_kernel(const __grid_constant__ StatsParams p) {
@@ -1397,9 +1428,14 @@ __global__ void __launch_bounds__(kThreads, 4)
     auto inc_of = [&](int pos) { return pos < roff ? 1u : (1u << 16); };
 
     // ================= order 1: tokens =================
-    for (int qi = tid; qi < nq; qi += kThreads) {  // round 1: claim home slots (plain stores)
-      int p0;
-      const uint32_t vm = quad(qi, p0);
+    // Only candidate tokens are inserted (store-then-verify); reference tokens
+    // look up: a reference token absent from the candidate can neither be
+    // counted (min(c, 0) = 0) nor start a matching n-gram.  Owners are
+    // therefore always candidate positions, and the table holds <= clen keys.
+    const int nrq = nq - ncq;
+    for (int qi = tid; qi < ncq; qi += kThreads) {  // round 1: claim home slots (plain stores)
+      const int p0 = 4 * qi;
+      const uint32_t vm = clen - p0 >= 4 ? 0xfu : ((1u << (clen - p0)) - 1u);
       T t[4];
       load4(p0, t);
 #pragma unroll
@@ -1409,9 +1445,9 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
     __syncthreads();
     TB_MARK(28);
-    for (int qi = tid; qi < nq; qi += kThreads) {  // round 2: verify
-      int p0;
-      const uint32_t vm = quad(qi, p0);
+    for (int qi = tid; qi < ncq; qi += kThreads) {  // round 2: verify
+      const int p0 = 4 * qi;
+      const uint32_t vm = clen - p0 >= 4 ? 0xfu : ((1u << (clen - p0)) - 1u);
       T t[4];
       load4(p0, t);
       uint32_t hv[4], home[4];
@@ -1429,7 +1465,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         const int pos = p0 + k;
         if ((vm >> k & 1u) && w[k] != pos) {
           if (tok[w[k]] == t[k]) {
-            atomicAdd(&cnt[w[k]], inc_of(pos));
+            atomicAdd(&cnt[w[k]], 1u);
           } else {
             lm |= 1u << k;
             pair_retry_store(own, hv[k], 1, hshift, static_cast<uint16_t>(pos));
@@ -1442,16 +1478,56 @@ __global__ void __launch_bounds__(kThreads, 4)
     __syncthreads();
     TB_MARK(29);
     TB_NOTE(27, s_nlost);
-    if (s_nlost)  // positions whose home slot holds another token
+    if (s_nlost)  // candidate positions whose home slot holds another token
       pair_resolve_lost(own, cnt, lost, s_nlost, id1, mask, hshift, roff, tid,
                         [&](uint16_t q) { return tok_hash32(tok[q]); },
                         [&](uint16_t a, uint16_t b) { return tok[a] == tok[b]; });
     TB_MARK(3);
-    {  // liveness + clipped count (added once per slot by its owner)
+    for (int qi = tid; qi < nrq; qi += kThreads) {  // reference lookups
+      const int p0 = roff + 4 * qi;
+      const uint32_t vm = roff + rlen - p0 >= 4 ? 0xfu : ((1u << (roff + rlen - p0)) - 1u);
+      T t[4];
+      load4(p0, t);
+      // the home slots of all four first (independent loads); the chain only
+      // when a home slot holds a different token
+      uint32_t hv[4], v[4];
+      uint16_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        hv[k] = tok_hash32(t[k]);
+        v[k] = hv[k] >> hshift;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = (vm >> k & 1u) ? own[v[k]] : static_cast<uint16_t>(0xffffu);
+      T to[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) to[k] = o[k] != 0xffffu ? tok[o[k]] : t[k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (o[k] != 0xffffu && to[k] != t[k]) {
+          const int sl = pair_find_retry(own, tok, t[k], hv[k], hshift, mask, &o[k]);
+          v[k] = static_cast<uint32_t>(sl);
+          if (sl < 0) o[k] = 0xffffu;
+        }
+        if (o[k] == 0xffffu) {
+          v[k] = 0xffffu;
+        } else {
+          atomicAdd(&cnt[o[k]], 1u << 16);
+          const int j = atomicAdd(&s_nsurv, 1);  // survivors are rare on unrelated text
+          if (j < 32) s_surv[j] = static_cast<uint16_t>(p0 + k);
+        }
+      }
+      const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+      *reinterpret_cast<uint2*>(id1 + p0) = vv;  // 0xffff: token absent from the candidate
+      *reinterpret_cast<uint2*>(idn + p0) = vv;
+    }
+    __syncthreads();
+    TB_MARK(26);
+    {  // candidate liveness + clipped count (added once per slot by its owner)
       unsigned int hits = 0;
-      for (int qi = tid; qi < nq; qi += kThreads) {
-        int p0;
-        const uint32_t vm = quad(qi, p0);
+      for (int qi = tid; qi < ncq; qi += kThreads) {
+        const int p0 = 4 * qi;
+        const uint32_t vm = clen - p0 >= 4 ? 0xfu : ((1u << (clen - p0)) - 1u);
         const uint2 s2 = *reinterpret_cast<const uint2*>(id1 + p0);
         const uint32_t s[4] = {s2.x & 0xffffu, s2.x >> 16, s2.y & 0xffffu, s2.y >> 16};
         uint32_t o[4], cw[4];
@@ -1465,13 +1541,12 @@ __global__ void __launch_bounds__(kThreads, 4)
           const int pos = p0 + k;
           v[k] = 0xffffu;
           if (vm >> k & 1u) {
-            const uint32_t c = (cw[k] & 0xffffu) + (o[k] < static_cast<uint32_t>(roff) ? 1u : 0u);
-            const uint32_t x = (cw[k] >> 16) + (o[k] >= static_cast<uint32_t>(roff) ? 1u : 0u);
-            const bool ok = pos < roff ? x != 0 : c != 0;
+            const uint32_t c = (cw[k] & 0xffffu) + 1u;  // the owner counts itself
+            const uint32_t x = cw[k] >> 16;
             if (o[k] == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
-            if (ok) {
+            if (x != 0) {
               v[k] = s[k];
-              const int j = atomicAdd(&s_nsurv, 1);  // survivors are rare on unrelated text
+              const int j = atomicAdd(&s_nsurv, 1);
               if (j < 32) s_surv[j] = static_cast<uint16_t>(pos);
             }
           }
@@ -1621,6 +1696,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       }
     }
 
+    TB_MARK(24);
     // ---- epilogue (warp 0)
     if (tid < 32) {
       const int64_t c = s_len[0];
