@@ -307,10 +307,10 @@ def run_ours(args):
     plan = plans[0]
 
     def step(pl):
-        """One step: the fused kernel (graph replay); in corpus mode across
+        """One step: the fused kernel (one launch); in corpus mode across
         ranks, then the NCCL all-reduce of the 2N+2 int64 totals over NVLink
         and the corpus epilogue on every rank."""
-        pl.replay()
+        pl.run()
         if corpus and world > 1:
             dist.all_reduce(pl.totals, op=dist.ReduceOp.SUM)
             pl.corpus_from_totals()
@@ -334,8 +334,6 @@ def run_ours(args):
 
     # ---- device-resident timing: K steps, back to back, each on its own batch
     stream = torch.cuda.current_stream(dev)
-    for pl in plans:
-        pl.capture()
     for k in range(max(args.warmup, 1) * len(plans)):
         step(plans[k % len(plans)])
     torch.cuda.synchronize(dev)
@@ -476,7 +474,7 @@ def run_ours(args):
             "config": {"workload": f"{args.workload}: {'corpus' if corpus else 'per-sentence'} BLEU-4, "
                                    f"B={b} L={l} V={v} R={r} smoothing={smoothing}, per GPU (weak scaling)",
                        "global_batch": b * world, "seq_len": l, "parallelism": f"dp{world} (row shards)",
-                       "timed_path": "SentenceBleuPlan CUDA-graph replay of tb_bleu_stats (1 kernel/step)"
+                       "timed_path": "SentenceBleuPlan.run(): one tb_bleu_stats launch per step (native binding)"
                                      + (", then NCCL all_reduce of the int64 totals + corpus epilogue kernel"
                                         if corpus and world > 1 else "")
                                      + "; K steps back to back between two CUDA events",

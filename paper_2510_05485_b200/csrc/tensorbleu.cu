@@ -329,7 +329,7 @@ __device__ void bleu_epilogue(const int64_t* num, const int64_t* den, int64_t c,
       if (n >= 1 && has_den) pn = __ddiv_rn(__dadd_rn(nd, kk), __dadd_rn(dd, kk));  // bleu.py:230-232
     } else if (smoothing == TB_SMOOTH_EXP) {
       if (zero_num) {                                         // bleu.py:234-238
-        pn = __ddiv_rn(1.0, __dmul_rn(exp2(counter), dd));
+        pn = __ddiv_rn(1.0, __dmul_rn(ldexp(1.0, static_cast<int>(counter)), dd));  // np.exp2 of an integer: exact
         counter = __dadd_rn(counter, 1.0);
       }
     }
@@ -377,30 +377,41 @@ __device__ __forceinline__ int64_t closest_ref_len(int64_t c, const int64_t* ref
 // order as bleu_epilogue / numpy: the log terms are summed sequentially by
 // lane 0.  All 32 lanes of the warp must call it.
 // --------------------------------------------------------------------------
+// brevity penalty, bleu.py:256-261 (1 if c > r, 0 if c == 0, else exp(1 - r/c))
+__device__ __forceinline__ double brevity_penalty_fp64(int64_t c, int64_t r) {
+  const double cd = static_cast<double>(c);
+  const double rd = static_cast<double>(r);
+  double bp = (cd > rd) ? 1.0 : exp(__dsub_rn(1.0, __ddiv_rn(rd, cd > 0.0 ? cd : 1.0)));
+  if (!(cd > 0.0)) bp = 0.0;
+  return bp;
+}
+
+// `bp_in` >= 0: the brevity penalty was computed beforehand (by another warp)
 __device__ void warp_epilogue(int64_t num, int64_t den, int64_t c, int64_t r, int N, int smoothing,
                               double eps, double kk, double w, double* prec_out, double* bp_out,
-                              double* score_out) {
+                              double* score_out, double bp_in = -1.0) {
   const int lane = threadIdx.x & 31;
   const bool act = lane < N;
   const double nd = static_cast<double>(num);
   const double dd = static_cast<double>(den);
   const bool has_den = act && den > 0;
   const bool zero_num = has_den && num == 0;
-  double pn = has_den ? __ddiv_rn(nd, dd) : 0.0;
+  // divisors of lanes without a denominator are replaced by 1: a division by 0
+  // takes the slow path of the fp64 divide (hundreds of cycles) even though its
+  // result is discarded
+  const double ds = has_den ? dd : 1.0;
+  double pn = has_den ? __ddiv_rn(nd, ds) : 0.0;
   if (smoothing == TB_SMOOTH_FLOOR) {
-    if (zero_num) pn = __ddiv_rn(eps, dd);
+    if (zero_num) pn = __ddiv_rn(eps, ds);
   } else if (smoothing == TB_SMOOTH_ADD_K) {
-    if (lane >= 1 && has_den) pn = __ddiv_rn(__dadd_rn(nd, kk), __dadd_rn(dd, kk));
+    if (lane >= 1 && has_den) pn = __ddiv_rn(__dadd_rn(nd, kk), __dadd_rn(ds, kk));
   } else if (smoothing == TB_SMOOTH_EXP) {
     const unsigned zb = __ballot_sync(kFull, zero_num);
     const double counter = 1.0 + static_cast<double>(__popc(zb & ((1u << lane) - 1u)));
-    if (zero_num) pn = __ddiv_rn(1.0, __dmul_rn(exp2(counter), dd));
+    if (zero_num) pn = __ddiv_rn(1.0, __dmul_rn(ldexp(1.0, static_cast<int>(counter)), ds));  // exact 2^counter
   }
   if (act && prec_out) prec_out[lane] = pn;
-  const double cd = static_cast<double>(c);
-  const double rd = static_cast<double>(r);
-  double bp = (cd > rd) ? 1.0 : exp(__dsub_rn(1.0, __ddiv_rn(rd, cd > 0.0 ? cd : 1.0)));
-  if (!(cd > 0.0)) bp = 0.0;
+  const double bp = bp_in >= 0.0 ? bp_in : brevity_penalty_fp64(c, r);
   const bool wpos = act && w > 0.0;
   const bool bad = __any_sync(kFull, wpos && !(pn > 0.0));  // an active precision is 0: score 0
   double score = 0.0;

@@ -67,23 +67,16 @@ class SentenceBleuPlan:
                 raise ValueError("unsupported shape for the device path")
             self.workspace = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 
-        def ld(t):
-            return t.stride(0) if t.shape[0] > 1 else t.shape[1]
-
         p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        self._ref_ids = (ctypes.c_void_p * R)(*[r.ids.data_ptr() for r in references])
-        self._ref_lens = (ctypes.c_void_p * R)(*[r.lengths.data_ptr() for r in references])
-        self._ref_ld = (ctypes.c_int64 * R)(*[ld(r.ids) for r in references])
-        self._ref_w = (ctypes.c_int64 * R)(*[int(w) for w in widths])
-        self._args = (
-            tb, candidates.ids.data_ptr(), ld(candidates.ids), candidates.max_len,
-            candidates.lengths.data_ptr(), R, self._ref_ids, self._ref_ld, self._ref_w, self._ref_lens,
-            B, N, _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k, _weights_arg(config),
-            p(self.numerators), p(self.denominators), p(self.cand_lens), p(self.eff_ref_lens),
-            p(self.scores), p(self.precisions), p(self.brevity_penalty),
-            p(self.totals), p(self.corpus), p(self.err),
-            p(self.workspace), self.workspace.numel())
-        self._fn = lib.tb_bleu_stats
+        # prebuilt arguments of the native launch (tb_bleu_stats through _hostpath)
+        want64 = tb == 8
+        views = tuple(b_._row_view(want64)[0] for b_ in (candidates, *references))
+        outs = (p(self.numerators), p(self.denominators), p(self.cand_lens), p(self.eff_ref_lens),
+                p(self.scores), p(self.precisions), p(self.brevity_penalty), p(self.totals), p(self.corpus))
+        self._launch_args = (views, B, N, _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k,
+                             ctypes.addressof(_weights_arg(config)), outs, p(self.err), p(self.workspace),
+                             self.workspace.numel())
+        self._hp = _native.hostpath()
         self.graph: Optional[torch.cuda.CUDAGraph] = None
 
     def corpus_from_totals(self) -> None:
@@ -104,7 +97,7 @@ class SentenceBleuPlan:
 
     def run(self) -> None:
         """Launch on the current stream (asynchronous)."""
-        rc = self._fn(*self._args, torch.cuda.current_stream(self.device).cuda_stream)
+        rc = self._hp.launch(*self._launch_args, _native.stream_handle(self.device))
         if rc:
             _native.check(rc, "tb_bleu_stats")
 
