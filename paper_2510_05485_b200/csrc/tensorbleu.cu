@@ -166,6 +166,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch (the stats kernels are launched with
+// programmatic stream serialization): wait until the preceding grid in the
+// stream has completed and its writes are visible — before the first global
+// read — then let the next grid start launching its CTAs into free SM slots,
+// where they do their own prologue and wait here in turn.  This hides the
+// kernel-to-kernel launch gap; without the launch attribute both are no-ops.
+__device__ __forceinline__ void griddep_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -516,6 +527,7 @@ __global__ void __launch_bounds__(kThreads)
     words = reinterpret_cast<W*>(g);
     keys = reinterpret_cast<int32_t*>(g + static_cast<size_t>(cap) * sizeof(W));
   }
+  griddep_wait_and_release();
 
   if (tid < 2 * N + 2) s_tot[tid] = 0;
   if (tid == 0) s_flags = 0;
@@ -884,6 +896,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     s_flags = 0;
     mbar_init(mbar, 1);
   }
+  griddep_wait_and_release();
   if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
   __syncthreads();
   TB_MARK(0);
@@ -1372,6 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     s_flags = 0;
     mbar_init(mbar, 1);
   }
+  griddep_wait_and_release();
   if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
   __syncthreads();
   TB_MARK(0);
@@ -2038,7 +2052,17 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
     const int64_t resident = static_cast<int64_t>(occ) * sms;
     grid = prm.batch < resident ? prm.batch : resident;
   }
-  kern<<<static_cast<unsigned>(grid), kThreads, pl.smem_bytes, stream>>>(prm);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TB_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }
