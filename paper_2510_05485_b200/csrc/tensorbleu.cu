@@ -1279,13 +1279,14 @@ __device__ __forceinline__ void pair_retry_store(uint16_t* own, uint32_t h, int 
 // The store half of round r+1 runs in the same pass as the verify half of
 // round r: stores only ever target EMPTY slots, and every slot being verified
 // in round r is non-empty, so the two halves cannot interfere.  The caller has
-// done the store half of round 1 (in its home-slot verify pass) and a barrier.
-// `ids[pos]` receives the final slot.  All threads call it.
+// done the store half of round 1 (in its home-slot verify pass) and a barrier
+// (with first_round > 1, rounds before it are complete and the store half of
+// first_round is done).  `ids[pos]` receives the final slot.  All threads call it.
 template <typename HashF, typename EqF>
 __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, uint16_t* lost, int nl, uint16_t* ids,
                                                   uint32_t mask, uint32_t hshift, int roff, int tid, HashF hash,
-                                                  EqF eq) {
-  for (int r = 1; r <= kRetryRounds; ++r) {
+                                                  EqF eq, int first_round = 1) {
+  for (int r = first_round; r <= kRetryRounds; ++r) {
     int left = 0;
     for (int i = tid; i < nl; i += kThreads) {
       const uint16_t pos = lost[i];
@@ -1352,7 +1353,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int64_t s_len[2];
   __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
   __shared__ int s_last, s_flags;
-  __shared__ int s_nlost, s_nsurv;
+  __shared__ int s_nlost, s_nsurv, s_ndef;
   __shared__ uint16_t s_surv[32];  // order-1 survivors when there are at most 32
   __shared__ int64_t s_stage_len[2];  // prefix mode: lengths read by issue_rows
 
@@ -1409,6 +1410,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     if (tid == 0) {
       s_nlost = 0;
       s_nsurv = 0;
+      s_ndef = 0;
     }
     copy_row_tails<T>(p, b, 2, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
     for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -1503,48 +1505,83 @@ __global__ void __launch_bounds__(kThreads, 4)
     __syncthreads();
     TB_MARK(29);
     TB_NOTE(27, s_nlost);
-    if (s_nlost)  // candidate positions whose home slot holds another token
-      pair_resolve_lost(own, cnt, lost, s_nlost, id1, mask, hshift, roff, tid,
-                        [&](uint16_t q) { return tok_hash32(tok[q]); },
-                        [&](uint16_t a, uint16_t b) { return tok[a] == tok[b]; });
-    TB_MARK(3);
-    for (int qi = tid; qi < nrq; qi += kThreads) {  // reference lookups
-      const int p0 = roff + 4 * qi;
-      const uint32_t vm = roff + rlen - p0 >= 4 ? 0xfu : ((1u << (roff + rlen - p0)) - 1u);
-      T t[4];
-      load4(p0, t);
-      // the home slots of all four first (independent loads); the chain only
-      // when a home slot holds a different token
-      uint32_t hv[4], v[4];
-      uint16_t o[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        hv[k] = tok_hash32(t[k]);
-        v[k] = hv[k] >> hshift;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) o[k] = (vm >> k & 1u) ? own[v[k]] : static_cast<uint16_t>(0xffffu);
-      T to[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) to[k] = o[k] != 0xffffu ? tok[o[k]] : t[k];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (o[k] != 0xffffu && to[k] != t[k]) {
-          const int sl = pair_find_retry(own, tok, t[k], hv[k], hshift, mask, &o[k]);
-          v[k] = static_cast<uint32_t>(sl);
-          if (sl < 0) o[k] = 0xffffu;
-        }
-        if (o[k] == 0xffffu) {
-          v[k] = 0xffffu;
+    {
+      // One pass: retry round 1 of the lost candidate positions (verify half,
+      // plus the store half of round 2) together with the home-slot lookups of
+      // every reference position.  A lookup is final when the home slot is
+      // EMPTY (the token has no candidate occurrence: lost keys never have an
+      // empty home) or holds the same token (home owners are fixed since
+      // round 1); a home held by a different token is deferred until the
+      // retry rounds have settled.  The store halves only fill EMPTY slots,
+      // and a home read EMPTY here stays conclusive for that token.
+      const int nl = s_nlost;
+      uint16_t* defl = lost + roff;  // deferred reference positions (capacity: padded ref width)
+      auto hash1 = [&](uint16_t q) { return tok_hash32(tok[q]); };
+      auto eq1 = [&](uint16_t a, uint16_t b) { return tok[a] == tok[b]; };
+      int left = 0;
+      for (int i = tid; i < nl; i += kThreads) {
+        const uint16_t pos = lost[i];
+        const uint32_t h = hash1(pos);
+        const uint32_t cs = rehash(h, 1, hshift);
+        const uint16_t w = own[cs];
+        if (w == pos || eq1(pos, w)) {
+          if (w != pos) atomicAdd(&cnt[w], 1u);
+          id1[pos] = static_cast<uint16_t>(cs);
+          lost[i] = 0xffffu;
         } else {
-          atomicAdd(&cnt[o[k]], 1u << 16);
-          const int j = atomicAdd(&s_nsurv, 1);  // survivors are rare on unrelated text
-          if (j < 32) s_surv[j] = static_cast<uint16_t>(p0 + k);
+          left = 1;
+          pair_retry_store(own, h, 2, hshift, pos);
         }
       }
-      const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
-      *reinterpret_cast<uint2*>(id1 + p0) = vv;  // 0xffff: token absent from the candidate
-      *reinterpret_cast<uint2*>(idn + p0) = vv;
+      for (int qi = tid; qi < nrq; qi += kThreads) {  // reference lookups (home slots)
+        const int p0 = roff + 4 * qi;
+        const uint32_t vm = roff + rlen - p0 >= 4 ? 0xfu : ((1u << (roff + rlen - p0)) - 1u);
+        T t[4];
+        load4(p0, t);
+        uint32_t v[4];
+        uint16_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = tok_hash32(t[k]) >> hshift;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = (vm >> k & 1u) ? own[v[k]] : static_cast<uint16_t>(0xffffu);
+        T to[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) to[k] = o[k] != 0xffffu ? tok[o[k]] : t[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (o[k] != 0xffffu && to[k] != t[k]) {  // home held by another token: later
+            defl[atomicAdd(&s_ndef, 1)] = static_cast<uint16_t>(p0 + k);
+            o[k] = 0xffffu;
+          }
+          if (o[k] == 0xffffu) {
+            v[k] = 0xffffu;
+          } else {
+            atomicAdd(&cnt[o[k]], 1u << 16);
+            const int j = atomicAdd(&s_nsurv, 1);  // survivors are rare on unrelated text
+            if (j < 32) s_surv[j] = static_cast<uint16_t>(p0 + k);
+          }
+        }
+        const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+        *reinterpret_cast<uint2*>(id1 + p0) = vv;  // 0xffff: token absent from the candidate
+        *reinterpret_cast<uint2*>(idn + p0) = vv;
+      }
+      if (__syncthreads_or(left))
+        pair_resolve_lost(own, cnt, lost, nl, id1, mask, hshift, roff, tid, hash1, eq1, 2);
+      TB_MARK(3);
+      const int nd = s_ndef;
+      for (int i = tid; i < nd; i += kThreads) {  // deferred lookups: the full chain
+        const uint16_t pos = defl[i];
+        const T t = tok[pos];
+        uint16_t o;
+        const int sl = pair_find_retry(own, tok, t, tok_hash32(t), hshift, mask, &o);
+        if (sl >= 0) {
+          atomicAdd(&cnt[o], 1u << 16);
+          id1[pos] = static_cast<uint16_t>(sl);
+          idn[pos] = static_cast<uint16_t>(sl);
+          const int j = atomicAdd(&s_nsurv, 1);
+          if (j < 32) s_surv[j] = pos;
+        }
+      }
     }
     __syncthreads();
     TB_MARK(26);
