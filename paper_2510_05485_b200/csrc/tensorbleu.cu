@@ -42,6 +42,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #define TB_VERSION_STRING "tensorbleu-b200 0.1.0 (sm_100a)"
 
@@ -1799,6 +1800,428 @@ __global__ void __launch_bounds__(kThreads, 4)
 }
 
 // --------------------------------------------------------------------------
+// Multi-reference kernel (2 <= R <= kMultiMaxRefs): the single-reference
+// design (candidate insert, reference lookups, retry rounds, quads) with one
+// u16 count per (reference, candidate owner) so that the clip is
+// min(cand, max_r ref_r) (bleu.py:148-157, oracle.py:36-37).  Every order,
+// including the pruned orders >= 2 when more than 32 positions stay live, runs
+// the same passes on its keys: order 1 on the tokens, order n on the packed
+// (prefix slot, last-token slot) keys.  All references are looked up in one
+// pass, so the number of barrier phases does not grow with R.
+//
+// Positions: candidate [0, cand_pad), reference r at cand_pad + ref_off[r]
+// (rows padded to 4).  cnt[o]: candidate count of owner o (owner excluded);
+// rc[r][o]: occurrences in reference r of the key owned by candidate position o.
+// --------------------------------------------------------------------------
+constexpr int kMultiMaxRefs = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 2)
+    bleu_multi_kernel(const __grid_constant__ StatsParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int s_hits[TB_MAX_ORDER];
+  __shared__ int64_t s_len[kMultiMaxRefs + 1];
+  __shared__ int64_t s_stage_len[kMultiMaxRefs + 1];
+  __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
+  __shared__ int s_last, s_flags;
+  __shared__ int s_nlost, s_nsurv, s_ndef;
+  __shared__ int s_qbase[kMultiMaxRefs + 2];  // first flattened reference quad of each reference (+ total)
+  __shared__ uint16_t s_surv[32];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int R = p.num_refs;
+  const int N = p.max_order;
+  const int cap_log2 = p.cap_log2;
+  const uint32_t cap = 1u << cap_log2;
+  const bool corpus = p.totals != nullptr || p.corpus != nullptr;
+  const int cpad = p.cand_pad;
+
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+  T* tok = reinterpret_cast<T*>(smem + 16);
+  uint32_t* kc = reinterpret_cast<uint32_t*>(smem + 16);           // aliases tok (orders >= 2)
+  uint16_t* id1 = reinterpret_cast<uint16_t*>(smem + p.off_id1);   // order-1 slot; 0xffff: token unmatched
+  uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot; 0xffff: n-gram unmatched
+  uint16_t* own = reinterpret_cast<uint16_t*>(smem + p.off_ent);   // slot -> owner (candidate) position
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + p.off_mref);  // candidate owner -> candidate count
+  uint32_t* rc = reinterpret_cast<uint32_t*>(smem + p.off_kc);     // (ref, candidate owner) -> u16 count, 2 per word
+  uint16_t* lost = reinterpret_cast<uint16_t*>(smem + p.off_lists);  // lost candidates [0, cpad), deferred refs after
+  uint16_t* defl = lost + cpad;
+  const uint32_t hshift = 32 - cap_log2;
+  const uint32_t mask = cap - 1;
+
+  auto issue_stage = [&](int64_t b) {
+    if (tid == 0) issue_rows<T>(p, b, R + 1, tok, mbar, s_stage_len, &s_flags);
+  };
+
+  if (tid < 2 * N + 2) s_tot[tid] = 0;
+  if (tid == 0) {
+    s_flags = 0;
+    mbar_init(mbar, 1);
+  }
+  griddep_wait_and_release();
+  if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
+  __syncthreads();
+  uint32_t phase = 0;
+
+  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    if (p.prefix_only) {
+      __syncthreads();  // s_stage_len of this group, written by thread 0 in issue_rows
+      if (tid <= R) s_len[tid] = s_stage_len[tid];
+    } else if (tid <= R) {
+      const int64_t len = tid == 0 ? p.cand_len[b] : p.refs[tid - 1].len[b];
+      const int64_t width = row_width(p, tid);
+      int64_t l = len;
+      if (len < 0 || len > width) {
+        atomicOr(&s_flags, TB_FLAG_BAD_LENGTH);
+        l = len < 0 ? 0 : width;
+      }
+      s_len[tid] = l;
+    }
+    if (tid < N) s_hits[tid] = 0;
+    copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    __syncthreads();
+    if (tid == 0) {
+      int q = 0;
+      for (int r = 0; r < R; ++r) {
+        s_qbase[r] = q;
+        q += static_cast<int>((s_len[r + 1] + 3) >> 2);
+      }
+      s_qbase[R] = q;
+    }
+
+    const int clen = static_cast<int>(s_len[0]);
+    const int ncq = (clen + 3) >> 2;
+    auto cand_mask = [&](int p0) -> uint32_t { return clen - p0 >= 4 ? 0xfu : ((1u << (clen - p0)) - 1u); };
+    // flattened reference quad -> (reference, first position, valid mask)
+    auto ref_quad = [&](int qi, int& r, int& p0) -> uint32_t {
+      r = 0;
+      while (r + 1 < R && qi >= s_qbase[r + 1]) ++r;
+      const int j = 4 * (qi - s_qbase[r]);
+      p0 = cpad + p.ref_off[r] + j;
+      const int left = static_cast<int>(s_len[r + 1]) - j;
+      return left >= 4 ? 0xfu : ((1u << left) - 1u);
+    };
+    auto row_end = [&](int pos) -> int {  // one past the last valid position of pos's row
+      if (pos < cpad) return clen;
+      int r = 0;
+      while (r + 1 < R && pos >= cpad + p.ref_off[r + 1]) ++r;
+      return cpad + p.ref_off[r] + static_cast<int>(s_len[r + 1]);
+    };
+    auto ref_of = [&](int pos) -> int {  // reference index of a reference position
+      int r = 0;
+      while (r + 1 < R && pos >= cpad + p.ref_off[r + 1]) ++r;
+      return r;
+    };
+    auto rc_add = [&](int r, uint32_t o) {
+      const uint32_t i = static_cast<uint32_t>(r * cpad) + o;
+      atomicAdd(&rc[i >> 1], 1u << (16 * (i & 1u)));
+    };
+    auto rc_max = [&](uint32_t o) -> uint32_t {
+      uint32_t x = 0;
+      for (int r = 0; r < R; ++r) {
+        const uint32_t i = static_cast<uint32_t>(r * cpad) + o;
+        const uint32_t v = (rc[i >> 1] >> (16 * (i & 1u))) & 0xffffu;
+        x = v > x ? v : x;
+      }
+      return x;
+    };
+    __syncthreads();  // s_qbase
+    const int nrq = s_qbase[R];
+
+    // One order: keys of the valid / live positions (K = token type at order 1,
+    // packed u32 keys after), ids -> slot or 0xffff.  Returns (via s_nsurv /
+    // s_surv) the live positions.  All threads call it.
+    auto count_order = [&](auto* keys, uint16_t* ids, uint16_t* ids2, int n, bool order1) {
+      using K = typename std::remove_const<typename std::remove_pointer<decltype(keys)>::type>::type;
+      auto load_keys = [&](int p0, K (&k)[4]) {
+        if constexpr (sizeof(K) == 4) {
+          const uint4 v = *reinterpret_cast<const uint4*>(keys + p0);
+          k[0] = static_cast<K>(v.x);
+          k[1] = static_cast<K>(v.y);
+          k[2] = static_cast<K>(v.z);
+          k[3] = static_cast<K>(v.w);
+        } else {
+          const longlong2 u = *reinterpret_cast<const longlong2*>(keys + p0);
+          const longlong2 v = *reinterpret_cast<const longlong2*>(keys + p0 + 2);
+          k[0] = u.x;
+          k[1] = u.y;
+          k[2] = v.x;
+          k[3] = v.y;
+        }
+      };
+      auto live_mask = [&](uint32_t vm, const K (&k)[4]) -> uint32_t {
+        if (order1) return vm;
+        uint32_t m = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if ((vm >> j & 1u) && static_cast<uint32_t>(k[j]) != ~0u) m |= 1u << j;
+        return m;
+      };
+      // table, candidate counts and per-reference counts start empty
+      for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      for (int i = tid; i < (R * cpad + 7) / 8; i += kThreads) reinterpret_cast<uint4*>(rc)[i] = make_uint4(0, 0, 0, 0);
+      if (tid == 0) {
+        s_nlost = 0;
+        s_ndef = 0;
+        s_nsurv = 0;
+      }
+      __syncthreads();
+      for (int qi = tid; qi < ncq; qi += kThreads) {  // claims (plain stores)
+        const int p0 = 4 * qi;
+        K k[4];
+        load_keys(p0, k);
+        const uint32_t vm = live_mask(cand_mask(p0), k);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (vm >> j & 1u) own[tok_hash32(k[j]) >> hshift] = static_cast<uint16_t>(p0 + j);
+        *reinterpret_cast<uint4*>(cnt + p0) = make_uint4(0, 0, 0, 0);
+      }
+      __syncthreads();
+      for (int qi = tid; qi < ncq; qi += kThreads) {  // verify
+        const int p0 = 4 * qi;
+        K k[4];
+        load_keys(p0, k);
+        const uint32_t vm = live_mask(cand_mask(p0), k);
+        uint32_t hv[4], home[4];
+        uint16_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          hv[j] = tok_hash32(k[j]);
+          home[j] = hv[j] >> hshift;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = (vm >> j & 1u) ? own[home[j]] : static_cast<uint16_t>(p0 + j);
+        uint32_t lm = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pos = p0 + j;
+          if (w[j] != pos) {
+            if (keys[w[j]] == k[j]) {
+              atomicAdd(&cnt[w[j]], 1u);
+            } else {
+              lm |= 1u << j;
+              pair_retry_store(own, hv[j], 1, hshift, static_cast<uint16_t>(pos));
+            }
+          }
+        }
+        *reinterpret_cast<uint2*>(ids + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
+        for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
+      }
+      __syncthreads();
+      const int nl = s_nlost;
+      auto hashk = [&](uint16_t q) { return tok_hash32(keys[q]); };
+      auto eqk = [&](uint16_t a, uint16_t c) { return keys[a] == keys[c]; };
+      int left = 0;
+      for (int i = tid; i < nl; i += kThreads) {  // retry round 1 (verify half) ...
+        const uint16_t pos = lost[i];
+        const uint32_t h = hashk(pos);
+        const uint32_t cs = rehash(h, 1, hshift);
+        const uint16_t w = own[cs];
+        if (w == pos || eqk(pos, w)) {
+          if (w != pos) atomicAdd(&cnt[w], 1u);
+          ids[pos] = static_cast<uint16_t>(cs);
+          lost[i] = 0xffffu;
+        } else {
+          left = 1;
+          pair_retry_store(own, h, 2, hshift, pos);
+        }
+      }
+      for (int qi = tid; qi < nrq; qi += kThreads) {  // ... with the home-slot lookups of all references
+        int r, p0;
+        const uint32_t vm0 = ref_quad(qi, r, p0);
+        K k[4];
+        load_keys(p0, k);
+        const uint32_t vm = live_mask(vm0, k);
+        uint32_t v[4];
+        uint16_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = tok_hash32(k[j]) >> hshift;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = (vm >> j & 1u) ? own[v[j]] : static_cast<uint16_t>(0xffffu);
+        K ko[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ko[j] = o[j] != 0xffffu ? keys[o[j]] : k[j];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (o[j] != 0xffffu && ko[j] != k[j]) {  // home held by another key: after the retries
+            defl[atomicAdd(&s_ndef, 1)] = static_cast<uint16_t>(p0 + j);
+            o[j] = 0xffffu;
+          }
+          if (o[j] == 0xffffu) {
+            v[j] = 0xffffu;
+          } else {
+            rc_add(r, o[j]);
+            const int s = atomicAdd(&s_nsurv, 1);
+            if (s < 32) s_surv[s] = static_cast<uint16_t>(p0 + j);
+          }
+        }
+        const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+        *reinterpret_cast<uint2*>(ids + p0) = vv;
+        if (ids2) *reinterpret_cast<uint2*>(ids2 + p0) = vv;
+      }
+      if (__syncthreads_or(left))
+        pair_resolve_lost(own, cnt, lost, nl, ids, mask, hshift, cpad, tid, hashk, eqk, 2);
+      const int nd = s_ndef;
+      for (int i = tid; i < nd; i += kThreads) {  // deferred lookups: the full chain
+        const uint16_t pos = defl[i];
+        const K key = keys[pos];
+        uint16_t o;
+        const int sl = pair_find_retry(own, keys, key, tok_hash32(key), hshift, mask, &o);
+        if (sl >= 0) {
+          rc_add(ref_of(pos), o);
+          ids[pos] = static_cast<uint16_t>(sl);
+          if (ids2) ids2[pos] = static_cast<uint16_t>(sl);
+          const int s = atomicAdd(&s_nsurv, 1);
+          if (s < 32) s_surv[s] = pos;
+        }
+      }
+      __syncthreads();
+      unsigned int hits = 0;
+      for (int qi = tid; qi < ncq; qi += kThreads) {  // candidate liveness + clipped count
+        const int p0 = 4 * qi;
+        K k[4];
+        load_keys(p0, k);
+        const uint32_t vm = live_mask(cand_mask(p0), k);
+        const uint2 s2 = *reinterpret_cast<const uint2*>(ids + p0);
+        const uint32_t s[4] = {s2.x & 0xffffu, s2.x >> 16, s2.y & 0xffffu, s2.y >> 16};
+        uint32_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pos = p0 + j;
+          v[j] = 0xffffu;
+          if (vm >> j & 1u) {
+            const uint32_t o = own[s[j]];
+            const uint32_t x = rc_max(o);
+            if (o == static_cast<uint32_t>(pos)) {
+              const uint32_t c = (cnt[o] & 0xffffu) + 1u;  // the owner counts itself
+              hits += c < x ? c : x;
+            }
+            if (x != 0) {
+              v[j] = s[j];
+              const int q = atomicAdd(&s_nsurv, 1);
+              if (q < 32) s_surv[q] = static_cast<uint16_t>(pos);
+            }
+          }
+        }
+        const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+        *reinterpret_cast<uint2*>(ids + p0) = vv;
+        if (ids2) *reinterpret_cast<uint2*>(ids2 + p0) = vv;
+      }
+      hits = __reduce_add_sync(kFull, hits);
+      if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+      __syncthreads();
+    };
+
+    // ================= order 1: tokens =================
+    count_order(static_cast<const T*>(tok), id1, idn, 1, true);
+    int nsurv = s_nsurv;
+
+    // ================= orders n >= 2 =================
+    int n = 2;
+    for (; n <= N && nsurv > 32; ++n) {
+      // packed keys of the positions whose (n-1)-prefix and last token are live
+      const int nq_all = ncq + nrq;
+      for (int qi = tid; qi < nq_all; qi += kThreads) {
+        int r = 0, p0 = 4 * qi;
+        const uint32_t vm = qi < ncq ? cand_mask(p0) : ref_quad(qi - ncq, r, p0);
+        const int end = row_end(p0);
+        uint32_t key[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pos = p0 + j;
+          key[j] = ~0u;
+          if (vm >> j & 1u) {
+            const uint16_t pre = idn[pos];
+            const int q = pos + n - 1;
+            if (pre != 0xffffu && q < end) {
+              const uint16_t last = id1[q];
+              if (last != 0xffffu) key[j] = (static_cast<uint32_t>(pre) << 16) | last;
+            }
+          }
+        }
+        *reinterpret_cast<uint4*>(kc + p0) = make_uint4(key[0], key[1], key[2], key[3]);
+      }
+      __syncthreads();
+      count_order(static_cast<const uint32_t*>(kc), idn, static_cast<uint16_t*>(nullptr), n, false);
+      nsurv = s_nsurv;
+    }
+    if (n <= N && nsurv > 0) {
+      // <= 32 live positions: warp 0 finishes the remaining orders with match.any
+      if (tid < 32) {
+        int pos = lane < nsurv ? s_surv[lane] : -1;
+        uint32_t pid = pos >= 0 ? idn[pos] : 0u;
+        const int side = pos < 0 ? -1 : (pos < cpad ? 0 : 1 + ref_of(pos));
+        const int end = pos < 0 ? 0 : row_end(pos);
+        for (int m = n; m <= N; ++m) {
+          bool valid = pos >= 0;
+          uint32_t key = 0;
+          if (valid) {
+            const int q = pos + m - 1;
+            valid = q < end && id1[q] != 0xffffu;
+            if (valid) key = (pid << 16) | id1[q];
+          }
+          const unsigned peers = __match_any_sync(kFull, valid ? key : 0xffffffffu - lane);
+          const unsigned c = __popc(peers & __ballot_sync(kFull, valid && side == 0));
+          unsigned x = 0;
+          for (int r = 0; r < R; ++r) {
+            const unsigned xr = __popc(peers & __ballot_sync(kFull, valid && side == r + 1));
+            x = xr > x ? xr : x;
+          }
+          const int leader = __ffs(peers) - 1;
+          unsigned h = (valid && lane == leader) ? (c < x ? c : x) : 0u;
+          h = __reduce_add_sync(kFull, h);
+          if (lane == 0) s_hits[m - 1] += h;
+          const bool ok = valid && (side == 0 ? x > 0 : c > 0);
+          if (!__any_sync(kFull, ok && side == 0)) break;
+          pos = ok ? pos : -1;
+          pid = static_cast<uint32_t>(leader);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+
+    // ---- epilogue (warp 0)
+    if (tid < 32) {
+      const int64_t c = s_len[0];
+      const int64_t num = lane < N ? static_cast<int64_t>(s_hits[lane]) : 0;
+      const int64_t den = (lane < N && c - lane > 0) ? c - lane : 0;
+      if (lane < N) {
+        if (p.num) p.num[b * N + lane] = num;
+        if (p.den) p.den[b * N + lane] = den;
+      }
+      const int64_t r = closest_ref_len(c, &s_len[1], R);
+      if (lane == 0) {
+        if (p.cand_len_out) p.cand_len_out[b] = c;
+        if (p.eff_ref) p.eff_ref[b] = r;
+      }
+      if (p.scores || p.precisions || p.bp)
+        warp_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, lane < N ? p.weights[lane] : 0.0,
+                      p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
+                      p.scores ? p.scores + b : nullptr);
+      if (corpus) {
+        if (lane < N) {
+          s_tot[lane] += static_cast<unsigned long long>(num);
+          s_tot[N + lane] += static_cast<unsigned long long>(den);
+        }
+        if (lane == 0) {
+          s_tot[2 * N] += static_cast<unsigned long long>(c);
+          s_tot[2 * N + 1] += static_cast<unsigned long long>(r);
+        }
+      }
+    }
+    if (b + gridDim.x < p.batch) {
+      __syncthreads();
+      issue_stage(b + gridDim.x);
+    }
+  }
+  finish_cta(p, s_tot, s_flags, s_last);
+}
+
+// --------------------------------------------------------------------------
 // Stand-alone epilogue / totals / validation kernels.
 // --------------------------------------------------------------------------
 struct EpiParams {
@@ -1907,7 +2330,8 @@ int dev_info(DevInfo** out) {
 // --------------------------------------------------------------------------
 struct Plan {
   bool smem_mode = false;
-  bool pair = false;  // single-reference kernel
+  bool pair = false;   // single-reference kernel
+  bool multi = false;  // multi-reference kernel
   int cap_log2 = 0;
   int cand_pad = 0;
   int ref_off[TB_MAX_REFS + 1] = {0};
@@ -1985,6 +2409,60 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       pl->off_ent = static_cast<int>(offs[2]);
       pl->off_mref = static_cast<int>(offs[3]);
       pl->off_lists = static_cast<int>(offs[4]);
+      pl->smem_bytes = static_cast<size_t>(total);
+      pl->ws_bytes = pl->acc_bytes;
+      return TB_OK;
+    }
+  }
+
+  // ---- multi-reference kernel layout (2 <= R <= kMultiMaxRefs)
+  if (R >= 2 && R <= kMultiMaxRefs) {
+    const int64_t cpad4 = round_up(cand_width, 4);
+    int64_t roff[TB_MAX_REFS + 1];
+    int64_t o = 0;
+    for (int r = 0; r < R; ++r) {
+      roff[r] = o;
+      o += round_up(ref_widths[r], 4);
+    }
+    roff[R] = o;
+    const int64_t ptot = cpad4 + o;
+    auto multi_layout = [&](int log2, int64_t* offs) {
+      const int64_t c = int64_t(1) << log2;
+      int64_t q = round_up(16 + ptot * (token_bytes > 4 ? token_bytes : 4), 16);
+      offs[0] = q;                          // id1
+      q = round_up(q + ptot * 2, 16);
+      offs[1] = q;                          // idn
+      q = round_up(q + ptot * 2, 16);
+      offs[2] = q;                          // own (u16 per slot)
+      q = round_up(q + c * 2, 16);
+      offs[3] = q;                          // cnt (u32 per candidate position)
+      q = round_up(q + cpad4 * 4, 16);
+      offs[4] = q;                          // rc (u16 per reference x candidate position)
+      q = round_up(q + R * cpad4 * 2, 16);
+      offs[5] = q;                          // lost candidates + deferred reference positions (u16)
+      q = round_up(q + ptot * 2, 16);
+      return q;
+    };
+    // table load <= 1/8 of the candidate positions while two CTAs fit per SM
+    int lg = cap_log2_for(8 * cpad4, 6);
+    int64_t offs[6];
+    int64_t total = multi_layout(lg, offs);
+    while (total + static_cast<int64_t>(kStaticSmemReserve) > smem_optin / 2 && (int64_t(1) << (lg - 1)) >= 2 * cpad4) {
+      --lg;
+      total = multi_layout(lg, offs);
+    }
+    if (lg <= 15 && ptot < 65535 && total + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin) {
+      pl->smem_mode = true;
+      pl->multi = true;
+      pl->cand_pad = static_cast<int>(cpad4);
+      pl->cap_log2 = lg;
+      for (int r = 0; r <= R; ++r) pl->ref_off[r] = static_cast<int>(roff[r]);
+      pl->off_id1 = static_cast<int>(offs[0]);
+      pl->off_idn = static_cast<int>(offs[1]);
+      pl->off_ent = static_cast<int>(offs[2]);
+      pl->off_mref = static_cast<int>(offs[3]);
+      pl->off_kc = static_cast<int>(offs[4]);
+      pl->off_lists = static_cast<int>(offs[5]);
       pl->smem_bytes = static_cast<size_t>(total);
       pl->ws_bytes = pl->acc_bytes;
       return TB_OK;
@@ -2109,6 +2587,10 @@ int launch_stats(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t s
   if (pl.pair) {
     static size_t attr_set[64] = {0};
     return launch_kernel(bleu_pair_kernel<T>, prm, pl, sms, true, attr_set, stream);
+  }
+  if (pl.multi) {
+    static size_t attr_set[64] = {0};
+    return launch_kernel(bleu_multi_kernel<T>, prm, pl, sms, true, attr_set, stream);
   }
   if (pl.smem_mode) {
     static size_t attr_set[64] = {0};
