@@ -1814,6 +1814,7 @@ __global__ void __launch_bounds__(kThreads, 4)
 // rc[r][o]: occurrences in reference r of the key owned by candidate position o.
 // --------------------------------------------------------------------------
 constexpr int kMultiMaxRefs = 8;
+constexpr int kSmallSet = 128;  // live positions finished without a table
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -1826,7 +1827,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ int s_last, s_flags;
   __shared__ int s_nlost, s_nsurv, s_ndef;
   __shared__ int s_qbase[kMultiMaxRefs + 2];  // first flattened reference quad of each reference (+ total)
-  __shared__ uint16_t s_surv[32];
+  __shared__ uint16_t s_surv[kSmallSet];   // live positions, when there are at most kSmallSet
+  __shared__ uint32_t s_skey[kSmallSet];   // small-set path: their keys at the current order
+  __shared__ uint8_t s_sside[kSmallSet];   // small-set path: 0 = candidate, 1 + r = reference r
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -1862,6 +1865,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   griddep_wait_and_release();
   if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
   __syncthreads();
+  TB_MARK(0);
   uint32_t phase = 0;
 
   for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
@@ -1883,6 +1887,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_wait(mbar, phase);
     phase ^= 1;
     __syncthreads();
+    TB_MARK(2);
     if (tid == 0) {
       int q = 0;
       for (int r = 0; r < R; ++r) {
@@ -1980,6 +1985,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         *reinterpret_cast<uint4*>(cnt + p0) = make_uint4(0, 0, 0, 0);
       }
       __syncthreads();
+      if (n == 1) TB_MARK(28);
       for (int qi = tid; qi < ncq; qi += kThreads) {  // verify
         const int p0 = 4 * qi;
         K k[4];
@@ -2011,6 +2017,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
       }
       __syncthreads();
+      if (n == 1) TB_MARK(29);
       const int nl = s_nlost;
       auto hashk = [&](uint16_t q) { return tok_hash32(keys[q]); };
       auto eqk = [&](uint16_t a, uint16_t c) { return keys[a] == keys[c]; };
@@ -2055,7 +2062,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           } else {
             rc_add(r, o[j]);
             const int s = atomicAdd(&s_nsurv, 1);
-            if (s < 32) s_surv[s] = static_cast<uint16_t>(p0 + j);
+            if (s < kSmallSet) s_surv[s] = static_cast<uint16_t>(p0 + j);
           }
         }
         const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
@@ -2064,6 +2071,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       if (__syncthreads_or(left))
         pair_resolve_lost(own, cnt, lost, nl, ids, mask, hshift, cpad, tid, hashk, eqk, 2);
+      if (n == 1) TB_MARK(3);
       const int nd = s_ndef;
       for (int i = tid; i < nd; i += kThreads) {  // deferred lookups: the full chain
         const uint16_t pos = defl[i];
@@ -2075,10 +2083,11 @@ __global__ void __launch_bounds__(kThreads, 2)
           ids[pos] = static_cast<uint16_t>(sl);
           if (ids2) ids2[pos] = static_cast<uint16_t>(sl);
           const int s = atomicAdd(&s_nsurv, 1);
-          if (s < 32) s_surv[s] = pos;
+          if (s < kSmallSet) s_surv[s] = pos;
         }
       }
       __syncthreads();
+      if (n == 1) TB_MARK(26);
       unsigned int hits = 0;
       for (int qi = tid; qi < ncq; qi += kThreads) {  // candidate liveness + clipped count
         const int p0 = 4 * qi;
@@ -2102,7 +2111,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (x != 0) {
               v[j] = s[j];
               const int q = atomicAdd(&s_nsurv, 1);
-              if (q < 32) s_surv[q] = static_cast<uint16_t>(pos);
+              if (q < kSmallSet) s_surv[q] = static_cast<uint16_t>(pos);
             }
           }
         }
@@ -2117,11 +2126,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     // ================= order 1: tokens =================
     count_order(static_cast<const T*>(tok), id1, idn, 1, true);
+    TB_MARK(4);
     int nsurv = s_nsurv;
 
     // ================= orders n >= 2 =================
     int n = 2;
-    for (; n <= N && nsurv > 32; ++n) {
+    for (; n <= N && nsurv > kSmallSet; ++n) {
       // packed keys of the positions whose (n-1)-prefix and last token are live
       const int nq_all = ncq + nrq;
       for (int qi = tid; qi < nq_all; qi += kThreads) {
@@ -2149,40 +2159,62 @@ __global__ void __launch_bounds__(kThreads, 2)
       nsurv = s_nsurv;
     }
     if (n <= N && nsurv > 0) {
-      // <= 32 live positions: warp 0 finishes the remaining orders with match.any
-      if (tid < 32) {
-        int pos = lane < nsurv ? s_surv[lane] : -1;
-        uint32_t pid = pos >= 0 ? idn[pos] : 0u;
-        const int side = pos < 0 ? -1 : (pos < cpad ? 0 : 1 + ref_of(pos));
-        const int end = pos < 0 ? 0 : row_end(pos);
-        for (int m = n; m <= N; ++m) {
-          bool valid = pos >= 0;
-          uint32_t key = 0;
-          if (valid) {
-            const int q = pos + m - 1;
-            valid = q < end && id1[q] != 0xffffu;
-            if (valid) key = (pid << 16) | id1[q];
-          }
-          const unsigned peers = __match_any_sync(kFull, valid ? key : 0xffffffffu - lane);
-          const unsigned c = __popc(peers & __ballot_sync(kFull, valid && side == 0));
-          unsigned x = 0;
-          for (int r = 0; r < R; ++r) {
-            const unsigned xr = __popc(peers & __ballot_sync(kFull, valid && side == r + 1));
-            x = xr > x ? xr : x;
-          }
-          const int leader = __ffs(peers) - 1;
-          unsigned h = (valid && lane == leader) ? (c < x ? c : x) : 0u;
-          h = __reduce_add_sync(kFull, h);
-          if (lane == 0) s_hits[m - 1] += h;
-          const bool ok = valid && (side == 0 ? x > 0 : c > 0);
-          if (!__any_sync(kFull, ok && side == 0)) break;
-          pos = ok ? pos : -1;
-          pid = static_cast<uint32_t>(leader);
+      // <= kSmallSet live positions: the remaining orders by direct comparison
+      // of their keys (S^2 / blockDim compares per thread, two barriers per
+      // order, no table).  An n-gram's id for the next order is the lowest
+      // index holding it.
+      const int S = nsurv;
+      int pos = -1, side = 0, end = 0;
+      uint32_t pid = 0;
+      if (tid < S) {
+        pos = s_surv[tid];
+        side = pos < cpad ? 0 : 1 + ref_of(pos);
+        end = row_end(pos);
+        pid = idn[pos];
+        s_sside[tid] = static_cast<uint8_t>(side);
+      }
+      for (int m = n; m <= N; ++m) {
+        bool valid = pos >= 0;
+        uint32_t key = 0xffffffffu - static_cast<uint32_t>(tid);  // unique for invalid entries
+        if (valid) {
+          const int q = pos + m - 1;
+          valid = q < end && id1[q] != 0xffffu;
+          if (valid) key = (pid << 16) | id1[q];
         }
-        __syncwarp();
+        if (tid < S) s_skey[tid] = key;
+        __syncthreads();
+        bool ok = false;
+        int leader = tid;
+        if (valid) {
+          unsigned c = 0;
+          unsigned xr[kMultiMaxRefs] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int j = 0; j < S; ++j) {
+            if (s_skey[j] != key) continue;
+            leader = j < leader ? j : leader;
+            const int sj = s_sside[j];
+            if (sj == 0) {
+              ++c;
+            } else {
+#pragma unroll
+              for (int r = 0; r < kMultiMaxRefs; ++r) xr[r] += (sj == r + 1) ? 1u : 0u;
+            }
+          }
+          unsigned x = 0;
+#pragma unroll
+          for (int r = 0; r < kMultiMaxRefs; ++r) x = xr[r] > x ? xr[r] : x;
+          if (leader == tid) {
+            const unsigned h = c < x ? c : x;
+            if (h) atomicAdd(&s_hits[m - 1], h);
+          }
+          ok = side == 0 ? x > 0 : c > 0;
+        }
+        if (!__syncthreads_or(ok && side == 0)) break;  // also: every key read before the next order
+        pos = ok ? pos : -1;
+        pid = static_cast<uint32_t>(leader);
       }
     }
     __syncthreads();
+    TB_MARK(24);
 
     // ---- epilogue (warp 0)
     if (tid < 32) {
@@ -2217,8 +2249,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncthreads();
       issue_stage(b + gridDim.x);
     }
+    TB_MARK(30);
   }
   finish_cta(p, s_tot, s_flags, s_last);
+  TB_MARK(31);
 }
 
 // --------------------------------------------------------------------------
