@@ -132,6 +132,15 @@ def hostpath():
 _cuda_ok: Optional[bool] = None
 
 
+def require_cuda_available() -> None:
+    global _cuda_ok
+    if _cuda_ok is None:
+        _cuda_ok = torch.cuda.is_available()
+    if not _cuda_ok:
+        raise RuntimeError("paper_2510_05485_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+
+
 def require_cuda(device: Optional[torch.device] = None) -> torch.device:
     global _cuda_ok
     if _cuda_ok is None:
@@ -178,6 +187,19 @@ def raise_flags(flags: int, what: str = "") -> None:
 
 
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def current_device_index() -> int:
+    """Index of torch's current CUDA device; raises without a GPU (no CPU fallback)."""
+    require_cuda_available()
+    return torch.cuda.current_device()
+
+
+def raw_stream(index: int) -> int:
+    """cudaStream_t of torch's current stream on device `index`."""
+    if _raw_stream is not None:
+        return _raw_stream(index)
+    return torch.cuda.current_stream(index).cuda_stream
 
 
 def stream_handle(device: torch.device) -> int:

@@ -163,19 +163,29 @@ def _launch_host(candidates: TokenBatch, references: Sequence[TokenBatch], confi
     """Host-buffer path: ONE blocking tb_bleu_host call through the native
     binding (_hostpath, GIL released).  Pinned token rows are read by the
     kernel over PCIe (valid prefixes only); results come back as numpy."""
-    hp = _native.hostpath()
-    device = _native.require_cuda()
-    batches = (candidates, *references)
-    want64 = any(b.ids.dtype not in _INT32 for b in batches)
-    views = tuple(b._row_view(want64)[0] for b in batches)
+    hp = _native._hp or _native.hostpath()
+    dev = _native.current_device_index()
+    want64 = candidates.ids.dtype not in _INT32
+    for b in references:
+        want64 = want64 or b.ids.dtype not in _INT32
+    views = (candidates._row_view(want64)[0], *[b._row_view(want64)[0] for b in references])
+    smc, eps, k, waddr = _config_abi(config)
     rc, flags, *outs = hp.run(_MODES[mode], views, candidates.batch_size, config.max_order,
-                              _native.SMOOTHING_CODES[config.smoothing], config.eps, config.k,
-                              _weights_addr(config), _native.stream_handle(device))
+                              smc, eps, k, waddr, _native.raw_stream(dev))
     if rc:
         _native.check(rc, "tb_bleu_host")
     if flags:
         _native.raise_flags(flags)
     return True, dict(zip(_OUT_NAMES[mode], outs)), None
+
+
+def _config_abi(config: BleuConfig):
+    """(smoothing code, eps, k, weights address) of a config, cached on it."""
+    v = config.__dict__.get("_abi")
+    if v is None:
+        v = (_native.SMOOTHING_CODES[config.smoothing], config.eps, config.k, _weights_addr(config))
+        object.__setattr__(config, "_abi", v)
+    return v
 
 
 _ws_bytes_cache: dict = {}

@@ -58,5 +58,46 @@ def main():
         print(f"{k:45s} median {med:8.1f} us   min {mn:8.1f} us")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] in ("native", "ncu")):
     main()
+
+
+def c2_native_vs_python():
+    """tb_bleu_host at c2 through the native binding with prebuilt views vs
+    the public sentence_bleu call (the difference is the Python layer)."""
+    from paper_2510_05485_b200 import _native, bleu
+    b, l, v, r, sm = bench.WORKLOADS["c2"]
+    cand, refs = bench.generate_batch(b, l, v, r)
+    cfg = tb.BleuConfig(smoothing=sm)
+    hc = tb.TokenBatch(ids=torch.from_numpy(cand[0].astype(np.int32)).pin_memory(), lengths=torch.from_numpy(cand[1]))
+    hr = [tb.TokenBatch(ids=torch.from_numpy(i.astype(np.int32)).pin_memory(), lengths=torch.from_numpy(ln))
+          for i, ln in refs]
+    hp = _native.hostpath()
+    views = tuple(x._row_view(False)[0] for x in [hc, *hr])
+    w = bleu._weights_addr(cfg)
+    s = _native.stream_handle(torch.device("cuda", 0))
+    print("c2 int32 sentence_bleu  median %8.1f us  min %8.1f us" % t_host(lambda: tb.sentence_bleu(hc, hr, cfg)))
+    print("c2 int32 hp.run direct  median %8.1f us  min %8.1f us" % t_host(lambda: hp.run(1, views, b, 4, 0, 0.1, 1.0, w, s)))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(20):
+        e0.record()
+        hp.run(1, views, b, 4, 0, 0.1, 1.0, w, s)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1000)
+    print("c2 int32 events around hp.run (GPU span) median %8.1f us" % float(np.median(ts)))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "native":
+    c2_native_vs_python()
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ncu":
+    from paper_2510_05485_b200 import _native, bleu
+    b, l, v, r, sm = bench.WORKLOADS["c2"]
+    cand, refs = bench.generate_batch(b, l, v, r)
+    cfg = tb.BleuConfig(smoothing=sm)
+    hc = tb.TokenBatch(ids=torch.from_numpy(cand[0].astype(np.int32)).pin_memory(), lengths=torch.from_numpy(cand[1]))
+    hr = [tb.TokenBatch(ids=torch.from_numpy(i.astype(np.int32)).pin_memory(), lengths=torch.from_numpy(ln))
+          for i, ln in refs]
+    for _ in range(10):
+        tb.sentence_bleu(hc, hr, cfg)

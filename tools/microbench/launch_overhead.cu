@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "tensorbleu.h"
@@ -106,5 +107,46 @@ int main() {
   cudaPointerAttributes a;
   printf("cudaPointerGetAttributes       %7.2f us\n", time_us([&] { cudaPointerGetAttributes(&a, h_ids); }));
   printf("sc=%f flags=%d\n", sc, flags);
+  {  // c2-shaped host call: 512 x 1024 int32 pinned rows, lengths U[512, 1024]
+    const int B2 = 512, L2 = 1024;
+    int32_t *hc, *hr;
+    int64_t *lc, *lr;
+    cudaHostAlloc(&hc, B2 * L2 * 4, 0);
+    cudaHostAlloc(&hr, B2 * L2 * 4, 0);
+    cudaHostAlloc(&lc, B2 * 8, 0);
+    cudaHostAlloc(&lr, B2 * 8, 0);
+    srand(3);
+    for (int i = 0; i < B2 * L2; ++i) {
+      hc[i] = rand() % 128000;
+      hr[i] = rand() % 128000;
+    }
+    for (int i = 0; i < B2; ++i) {
+      lc[i] = 512 + rand() % 513;
+      lr[i] = 512 + rand() % 513;
+    }
+    std::vector<double> scores(B2);
+    const void* r2[1] = {hr};
+    const int64_t* l2[1] = {lr};
+    int64_t ld2[1] = {L2}, w2[1] = {L2};
+    auto call = [&] {
+      tb_bleu_host(4, hc, L2, L2, lc, 1, r2, ld2, w2, l2, B2, N, 0, 0.1, 1.0, wts, nullptr, nullptr, nullptr,
+                   nullptr, scores.data(), nullptr, nullptr, nullptr, nullptr, &flags, st);
+    };
+    printf("tb_bleu_host c2 int32 pinned   %7.2f us\n", time_us(call, 200));
+    cudaEvent_t a, b2;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b2);
+    float tot = 0;
+    for (int i = 0; i < 50; ++i) {
+      cudaEventRecord(a, st);
+      call();
+      cudaEventRecord(b2, st);
+      cudaEventSynchronize(b2);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b2);
+      tot += ms;
+    }
+    printf("  (events around it: %7.2f us)\n", tot * 1000 / 50);
+  }
   return 0;
 }
