@@ -41,9 +41,11 @@ METRIC = "per-sentence BLEU-4 sentences/sec at 512x1024 tok; HBM roofline %; vs 
 L2_FLUSH_BYTES = 256 << 20
 
 
-def generate_batch(b, l, v, r, seed=42):
+def generate_batch(b, l, v, r, seed=42, data="uniform"):
     """The reference generator, bench.py:72-91: default_rng([seed, B, L, V]),
-    IDs uniform in [0, V), lengths uniform in [L/2, L]; candidates then refs."""
+    IDs uniform in [0, V), lengths uniform in [L/2, L]; candidates then refs.
+    data="correlated" (SURVEY §8d parity input): every reference is the
+    candidate with a per-row mutation rate p ~ U[0, 0.9] and length +-50."""
     rng = np.random.default_rng([seed, b, l, v])
 
     def draw():
@@ -52,7 +54,16 @@ def generate_batch(b, l, v, r, seed=42):
         return ids, lengths
 
     cand = draw()
-    return cand, [draw() for _ in range(r)]
+    if data == "uniform":
+        return cand, [draw() for _ in range(r)]
+    refs = []
+    for _ in range(r):
+        ids = cand[0].copy()
+        m = rng.random((b, l)) < rng.uniform(0.0, 0.9, (b, 1))
+        ids[m] = rng.integers(0, v, size=int(m.sum()))
+        lengths = np.clip(cand[1] + rng.integers(-50, 51, size=b), l // 2, l)
+        refs.append((ids, lengths))
+    return cand, refs
 
 
 def algorithmic_bytes(lengths_rows, v, b, max_order=4):
@@ -278,7 +289,7 @@ def run_ours(args):
     b, l, v, r, smoothing = WORKLOADS[args.workload]
     mode = MODES.get(args.workload, "sentence")
     corpus = mode == "corpus"
-    cand_np, refs_np = generate_batch(b, l, v, r, seed=42 + rank)
+    cand_np, refs_np = generate_batch(b, l, v, r, seed=42 + rank, data=args.data)
     cfg = tb.BleuConfig(smoothing=smoothing)
     mk_plan = (lambda c_, r_: tb.SentenceBleuPlan(c_, r_, cfg, stats=False, corpus=True, sentence=False)) \
         if corpus else (lambda c_, r_: tb.SentenceBleuPlan(c_, r_, cfg))
@@ -303,7 +314,15 @@ def run_ours(args):
             lens = torch.randint(l // 2, l + 1, (b,), generator=gen, device=dev, dtype=torch.int64)
             return tb.TokenBatch.trusted(ids, lens)
 
-        plans.append(mk_plan(draw(), [draw() for _ in range(r)]))
+        def mutate(c_):
+            p_ = torch.rand((b, 1), generator=gen, device=dev) * 0.9
+            m_ = torch.rand((b, l), generator=gen, device=dev) < p_
+            ids = torch.where(m_, torch.randint(0, v, (b, l), generator=gen, device=dev, dtype=torch.int32), c_.ids)
+            lens = (c_.lengths + torch.randint(-50, 51, (b,), generator=gen, device=dev)).clamp(l // 2, l)
+            return tb.TokenBatch.trusted(ids, lens)
+
+        c_k = draw()
+        plans.append(mk_plan(c_k, [draw() if args.data == "uniform" else mutate(c_k) for _ in range(r)]))
     plan = plans[0]
 
     def step(pl):
@@ -470,7 +489,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic (reference generate_batch: uniform IDs, lengths U[L/2, L], seed 42+rank)",
+            "data": ("synthetic (reference generate_batch: uniform IDs, lengths U[L/2, L], seed 42+rank)"
+                     if args.data == "uniform" else
+                     "synthetic, correlated: references = candidate with per-row mutation rate U[0, 0.9]"),
             "config": {"workload": f"{args.workload}: {'corpus' if corpus else 'per-sentence'} BLEU-4, "
                                    f"B={b} L={l} V={v} R={r} smoothing={smoothing}, per GPU (weak scaling)",
                        "global_batch": b * world, "seq_len": l, "parallelism": f"dp{world} (row shards)",
@@ -519,6 +540,8 @@ def main(argv=None):
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--data", choices=["uniform", "correlated"], default="uniform",
+                   help="uniform = the reference generator (the headline); correlated = related references")
     p.add_argument("--clock-window", type=float, default=1.5,
                    help="seconds of sustained load sampled by nvidia-smi before the timed steps")
     args = p.parse_args(argv)
