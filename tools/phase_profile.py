@@ -32,9 +32,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--dtype", default="int32")
+    ap.add_argument("--data", default="uniform")
     args = ap.parse_args()
     b, l, v, r, sm = bench.WORKLOADS[args.workload]
-    (cid, clen), refs = bench.generate_batch(b, l, v, r)
+    (cid, clen), refs = bench.generate_batch(b, l, v, r, data=args.data)
     dt = torch.int32 if args.dtype == "int32" else torch.int64
     cand = tb.TokenBatch(ids=torch.as_tensor(cid).cuda().to(dt), lengths=torch.as_tensor(clen).cuda())
     rb = [tb.TokenBatch(ids=torch.as_tensor(i).cuda().to(dt), lengths=torch.as_tensor(ln).cuda()) for i, ln in refs]
