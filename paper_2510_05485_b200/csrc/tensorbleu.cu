@@ -1357,6 +1357,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int s_nlost, s_nsurv, s_ndef;
   __shared__ uint16_t s_surv[32];  // order-1 survivors when there are at most 32
   __shared__ int64_t s_stage_len[2];  // prefix mode: lengths read by issue_rows
+  __shared__ double s_bp;             // brevity penalty of the current group
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -1503,6 +1504,10 @@ __global__ void __launch_bounds__(kThreads, 4)
       *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
       for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
     }
+    // the brevity penalty depends on the lengths only: the last warp (idle in the
+    // candidate passes unless the candidate has > 7/8 * 4 * blockDim tokens)
+    // computes it here, off the critical path of the epilogue
+    if (tid == kThreads - 32) s_bp = brevity_penalty_fp64(s_len[0], s_len[1]);
     __syncthreads();
     TB_MARK(29);
     TB_NOTE(27, s_nlost);
@@ -1777,7 +1782,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       if (p.scores || p.precisions || p.bp)
         warp_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, lane < N ? p.weights[lane] : 0.0,
                       p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
-                      p.scores ? p.scores + b : nullptr);
+                      p.scores ? p.scores + b : nullptr, s_bp);
       if (corpus) {
         if (lane < N) {
           s_tot[lane] += static_cast<unsigned long long>(num);
