@@ -180,3 +180,34 @@ def test_buffer_api_empty_batch_needs_no_device():
     out = ext.score_sentences(np.zeros((0, 4), dtype=np.int64), np.zeros(0, dtype=np.int64),
                               np.zeros((1, 0, 4), dtype=np.int64), np.zeros((1, 0), dtype=np.int64))
     assert out.shape == (0,) and out.dtype == np.float64
+
+
+# --- the native host-path binding (_hostpath): argument checks before any device call
+def test_hostpath_binding_loads_and_checks_arguments():
+    hp = _native.hostpath()
+    good = (0, 4, 4, 0, 8)
+    with pytest.raises(TypeError):
+        hp.run(1, (good,))                                    # wrong arity
+    with pytest.raises(ValueError):
+        hp.run(1, (good,), 1, 4, 0, 0.1, 1.0, 0, 0)          # no reference view
+    with pytest.raises(TypeError):
+        hp.run(1, (good, (0, 4)), 1, 4, 0, 0.1, 1.0, 0, 0)  # malformed view
+    with pytest.raises(ValueError):
+        hp.run(1, (good, good), -1, 4, 0, 0.1, 1.0, 0, 0)   # negative batch
+    with pytest.raises(ValueError):
+        hp.run(1, (good, good), 1, 0, 0, 0.1, 1.0, 0, 0)    # max_order 0
+    with pytest.raises(ValueError):
+        hp.run(1, (good, (0, 4, 4, 0, 4)), 1, 4, 0, 0.1, 1.0, 0, 0)  # mixed token widths
+    with pytest.raises(ValueError):
+        hp.launch((good,), 1, 4, 0, 0.1, 1.0, 0, (None,) * 9, 0, 0, 0, 0)
+
+
+def test_row_views_are_cached_and_widened_once():
+    b = tb.TokenBatch(ids=np.arange(12, dtype=np.int64).reshape(3, 4), lengths=np.array([4, 2, 0]))
+    v1, keep = b._row_view(True)
+    assert v1[1:3] == (4, 4) and v1[4] == 8 and b._row_view(True)[0] is v1
+    import torch
+    b32 = tb.TokenBatch(ids=torch.arange(12, dtype=torch.int32).reshape(3, 4), lengths=torch.tensor([4, 2, 0]))
+    assert b32._row_view(False)[0][4] == 4
+    w = b32._row_view(True)
+    assert w[0][4] == 8 and w[1][0].dtype == torch.int64  # widened copy kept alive with the view
