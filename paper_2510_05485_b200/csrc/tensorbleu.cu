@@ -1835,6 +1835,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ uint16_t s_surv[kSmallSet];   // live positions, when there are at most kSmallSet
   __shared__ uint32_t s_skey[kSmallSet];   // small-set path: their keys at the current order
   __shared__ uint8_t s_sside[kSmallSet];   // small-set path: 0 = candidate, 1 + r = reference r
+  __shared__ int64_t s_effref;             // effective reference length of the current group
+  __shared__ double s_bp;                  // and its brevity penalty
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -2020,6 +2022,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         *reinterpret_cast<uint2*>(ids + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
         for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
+      }
+      if (order1 && tid == kThreads - 32) {  // lengths only: the last warp, off the epilogue's critical path
+        const int64_t r = closest_ref_len(s_len[0], &s_len[1], R);
+        s_effref = r;
+        s_bp = brevity_penalty_fp64(s_len[0], r);
       }
       __syncthreads();
       if (n == 1) TB_MARK(29);
@@ -2230,7 +2237,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (p.num) p.num[b * N + lane] = num;
         if (p.den) p.den[b * N + lane] = den;
       }
-      const int64_t r = closest_ref_len(c, &s_len[1], R);
+      const int64_t r = s_effref;
       if (lane == 0) {
         if (p.cand_len_out) p.cand_len_out[b] = c;
         if (p.eff_ref) p.eff_ref[b] = r;
@@ -2238,7 +2245,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (p.scores || p.precisions || p.bp)
         warp_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, lane < N ? p.weights[lane] : 0.0,
                       p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
-                      p.scores ? p.scores + b : nullptr);
+                      p.scores ? p.scores + b : nullptr, s_bp);
       if (corpus) {
         if (lane < N) {
           s_tot[lane] += static_cast<unsigned long long>(num);
