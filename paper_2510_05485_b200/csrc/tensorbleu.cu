@@ -49,6 +49,8 @@
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMultiMaxRefs = 8;  // references handled by the multi-reference kernel
+constexpr int kSmallSet = 128;    // positions matched without a table (<= kThreads)
 constexpr int kAccCopies = 32;         // replicated corpus accumulators (spread L2 atomics)
 constexpr int kGlobalKeyShift = 26;    // global-mode key = (ref << 26) | position
 constexpr uint32_t kFull = 0xffffffffu;
@@ -1354,8 +1356,9 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int64_t s_len[2];
   __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
   __shared__ int s_last, s_flags;
-  __shared__ int s_nlost, s_nsurv, s_ndef;
-  __shared__ uint16_t s_surv[32];  // order-1 survivors when there are at most 32
+  __shared__ int s_nlost, s_nsurv, s_ndef, s_nf;
+  __shared__ uint16_t s_flist[kSmallSet];  // positions that pass the order-1 filter
+  __shared__ uint16_t s_surv[kSmallSet];  // order-1 survivors (the first kSmallSet)
   __shared__ int64_t s_stage_len[2];  // prefix mode: lengths read by issue_rows
   __shared__ double s_bp;             // brevity penalty of the current group
 
@@ -1393,6 +1396,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   __syncthreads();
   TB_MARK(0);
   uint32_t phase = 0;
+  bool try_filter = true;  // off after a group of this CTA needed the hash passes (related text)
 
   for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
     if (p.prefix_only) {
@@ -1413,9 +1417,14 @@ __global__ void __launch_bounds__(kThreads, 4)
       s_nlost = 0;
       s_nsurv = 0;
       s_ndef = 0;
+      s_nf = 0;
     }
     copy_row_tails<T>(p, b, 2, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
-    for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    // the table region starts as the two filter bitmaps (zero) or as the empty table
+    {
+      const uint32_t fill = try_filter ? 0u : ~0u;
+      for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(fill, fill, fill, fill);
+    }
     mbar_wait(mbar, phase);
     phase ^= 1;
     __syncthreads();
@@ -1456,6 +1465,124 @@ __global__ void __launch_bounds__(kThreads, 4)
     };
     auto inc_of = [&](int pos) { return pos < roff ? 1u : (1u << 16); };
 
+    // ================= order 1: filter =================
+    // Each side marks its tokens in a two-hash Bloom filter (the table region:
+    // 8 bits per slot per side, <= 1/16 of the bits set per side); a token not
+    // in the other side's filter cannot match (false positives ~0.1%).  When at most kSmallSet positions pass (unrelated
+    // text: the ~1% that match plus ~1% false positives), their tokens are
+    // matched exactly among themselves — one warp with match.any up to 32, the
+    // block by direct comparison up to kSmallSet — and the hash passes below are
+    // skipped.  Otherwise (related text) the table is reset and they run.
+    bool filtered = false;
+    if (try_filter) {
+      uint32_t* bmc = reinterpret_cast<uint32_t*>(own);  // candidate tokens
+      uint32_t* bmr = bmc + cap / 4;                      // reference tokens
+      const uint32_t fshift = hshift - 3;                 // cap * 8 bits per bitmap
+      for (int qi = tid; qi < nq; qi += kThreads) {
+        int p0;
+        const uint32_t vm = quad(qi, p0);
+        T t[4];
+        load4(p0, t);
+        uint32_t* bm = p0 < roff ? bmc : bmr;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (vm >> k & 1u) {
+            const uint32_t h = tok_hash32(t[k]);
+            const uint32_t h1 = h >> fshift, h2 = (h * 0x85EBCA6Bu) >> fshift;
+            atomicOr(&bm[h1 >> 5], 1u << (h1 & 31u));
+            atomicOr(&bm[h2 >> 5], 1u << (h2 & 31u));
+          }
+      }
+      __syncthreads();
+      TB_MARK(20);
+      for (int qi = tid; qi < nq; qi += kThreads) {
+        int p0;
+        const uint32_t vm = quad(qi, p0);
+        T t[4];
+        load4(p0, t);
+        const uint32_t* bm = p0 < roff ? bmr : bmc;  // the other side's
+        uint32_t pm = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (vm >> k & 1u) {
+            const uint32_t h = tok_hash32(t[k]);
+            const uint32_t h1 = h >> fshift, h2 = (h * 0x85EBCA6Bu) >> fshift;
+            if ((bm[h1 >> 5] >> (h1 & 31u) & 1u) && (bm[h2 >> 5] >> (h2 & 31u) & 1u)) pm |= 1u << k;
+          }
+        // every valid position starts "unmatched" at order 1 (the exact match below
+        // marks the matched ones)
+        *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
+        *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
+        for (; pm; pm &= pm - 1) {
+          const int j = atomicAdd(&s_nf, 1);
+          if (j < kSmallSet) s_flist[j] = static_cast<uint16_t>(p0 + __ffs(pm) - 1);
+        }
+      }
+      __syncthreads();
+      TB_MARK(21);
+      TB_NOTE(25, s_nf);
+      const int S = s_nf;
+      if (S <= kSmallSet && tid == kThreads - 32)  // the last warp is idle below
+        s_bp = brevity_penalty_fp64(s_len[0], s_len[1]);
+      if (S <= 32) {
+        filtered = true;
+        if (tid < 32) {  // exact order-1 match of the S listed positions
+          const int pos = lane < S ? static_cast<int>(s_flist[lane]) : -1;
+          const T t = pos >= 0 ? tok[pos] : T(0);
+          const unsigned peers = __match_any_sync(kFull, pos >= 0 ? t : static_cast<T>(-1 - lane));
+          const unsigned c = __popc(peers & __ballot_sync(kFull, pos >= 0 && pos < roff));
+          const unsigned x = __popc(peers & __ballot_sync(kFull, pos >= roff));
+          const int leader = __ffs(peers) - 1;
+          unsigned h = (pos >= 0 && lane == leader) ? (c < x ? c : x) : 0u;
+          h = __reduce_add_sync(kFull, h);
+          const bool live = pos >= 0 && (pos < roff ? x > 0 : c > 0);
+          if (live) {
+            id1[pos] = static_cast<uint16_t>(leader);
+            idn[pos] = static_cast<uint16_t>(leader);
+          }
+          const unsigned lm = __ballot_sync(kFull, live);
+          if (live) s_surv[__popc(lm & ((1u << lane) - 1u))] = static_cast<uint16_t>(pos);
+          if (lane == 0) {
+            s_hits[0] = h;
+            s_nsurv = __popc(lm);
+          }
+        }
+      } else if (S <= kSmallSet) {
+        filtered = true;  // the block compares the S listed tokens directly
+        const int pos = tid < S ? static_cast<int>(s_flist[tid]) : -1;
+        bool live = false;
+        if (pos >= 0) {
+          const T t = tok[pos];
+          unsigned c = 0, x = 0;
+          int leader = tid;
+          for (int j = 0; j < S; ++j) {
+            const int q = s_flist[j];
+            if (tok[q] != t) continue;
+            leader = j < leader ? j : leader;
+            if (q < roff) ++c; else ++x;
+          }
+          if (leader == tid) {
+            const unsigned h = c < x ? c : x;
+            if (h) atomicAdd(&s_hits[0], h);
+          }
+          live = pos < roff ? x > 0 : c > 0;
+          if (live) {
+            id1[pos] = static_cast<uint16_t>(leader);
+            idn[pos] = static_cast<uint16_t>(leader);
+            const int j = atomicAdd(&s_nsurv, 1);
+            if (j < kSmallSet) s_surv[j] = static_cast<uint16_t>(pos);
+          }
+        }
+      } else {  // related text: reset the table region for the hash passes
+        for (uint32_t s = tid; s < cap / 8; s += kThreads)
+          reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        try_filter = false;  // uniform across the CTA (S is)
+      }
+      __syncthreads();
+      TB_MARK(22);
+    }
+
+    if (!filtered) {
     // ================= order 1: tokens =================
     // Only candidate tokens are inserted (store-then-verify); reference tokens
     // look up: a reference token absent from the candidate can neither be
@@ -1627,6 +1754,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       if (lane == 0 && hits) atomicAdd(&s_hits[0], hits);
     }
     __syncthreads();
+    }
     TB_MARK(4);
     int nsurv = s_nsurv;
 
@@ -1818,8 +1946,6 @@ __global__ void __launch_bounds__(kThreads, 4)
 // (rows padded to 4).  cnt[o]: candidate count of owner o (owner excluded);
 // rc[r][o]: occurrences in reference r of the key owned by candidate position o.
 // --------------------------------------------------------------------------
-constexpr int kMultiMaxRefs = 8;
-constexpr int kSmallSet = 128;  // live positions finished without a table
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 2)

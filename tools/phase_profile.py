@@ -26,6 +26,7 @@ for n in range(2, 7):
     for k, nm in enumerate(["P0clear", "P1cand", "P2ref", "P3live"]):
         NAMES.setdefault(3 + 4 * (n - 1) + k, f"o{n}.{nm}")
 NAMES[24] = "orders>=2"
+NAMES.update({20: "f.bitmaps", 21: "f.filter", 22: "f.match"})
 
 
 def main():
@@ -72,8 +73,10 @@ def main():
     print(f"CTAs {grid}; CTA start spread {np.ptp(t[:, 0])} ns; first start -> last finish "
           f"{t[:, 31].max() - t0} ns")
     print(f"order-1 deferred inserts per CTA: mean {t[:, 27].mean():.1f} max {t[:, 27].max()}")
+    print(f"filter passes per CTA: mean {t[:, 25].mean():.1f} max {t[:, 25].max()}")
     t[:, 27] = 0
-    for k in [0, 1, 2, 28, 29, 3, 26, 4] + list(range(5, 24)) + [25] + [24, 30, 31]:
+    t[:, 25] = 0
+    for k in [0, 1, 2, 20, 21, 22, 28, 29, 3, 26, 4] + list(range(5, 20)) + [23, 24, 30, 31]:
         col = t[:, k]
         ok = col > 0
         if not ok.any():
