@@ -1466,18 +1466,24 @@ __global__ void __launch_bounds__(kThreads, 4)
     auto inc_of = [&](int pos) { return pos < roff ? 1u : (1u << 16); };
 
     // ================= order 1: filter =================
-    // Each side marks its tokens in a two-hash Bloom filter (the table region:
-    // 8 bits per slot per side, <= 1/16 of the bits set per side); a token not
-    // in the other side's filter cannot match (false positives ~0.1%).  When at most kSmallSet positions pass (unrelated
+    // Each side marks its tokens in a blocked two-bit Bloom filter (the table
+    // region: a 32-bit word per 4 slots per side, both bits of a token in one
+    // word); a token not in the other side's filter cannot match (false
+    // positives ~0.1% at the table's load).  When at most kSmallSet positions pass (unrelated
     // text: the ~1% that match plus ~1% false positives), their tokens are
     // matched exactly among themselves — one warp with match.any up to 32, the
     // block by direct comparison up to kSmallSet — and the hash passes below are
     // skipped.  Otherwise (related text) the table is reset and they run.
     bool filtered = false;
     if (try_filter) {
+      // blocked: both bits of a token in one 32-bit word (one atomic / one load)
       uint32_t* bmc = reinterpret_cast<uint32_t*>(own);  // candidate tokens
       uint32_t* bmr = bmc + cap / 4;                      // reference tokens
-      const uint32_t fshift = hshift - 3;                 // cap * 8 bits per bitmap
+      const uint32_t wshift = hshift + 2;                 // cap / 4 words per filter
+      auto fmask = [](uint32_t h) {
+        const uint32_t g = h * 0x85EBCA6Bu;
+        return (1u << (g >> 27)) | (1u << ((g >> 22) & 31u));
+      };
       for (int qi = tid; qi < nq; qi += kThreads) {
         int p0;
         const uint32_t vm = quad(qi, p0);
@@ -1488,9 +1494,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         for (int k = 0; k < 4; ++k)
           if (vm >> k & 1u) {
             const uint32_t h = tok_hash32(t[k]);
-            const uint32_t h1 = h >> fshift, h2 = (h * 0x85EBCA6Bu) >> fshift;
-            atomicOr(&bm[h1 >> 5], 1u << (h1 & 31u));
-            atomicOr(&bm[h2 >> 5], 1u << (h2 & 31u));
+            atomicOr(&bm[h >> wshift], fmask(h));
           }
       }
       __syncthreads();
@@ -1506,8 +1510,8 @@ __global__ void __launch_bounds__(kThreads, 4)
         for (int k = 0; k < 4; ++k)
           if (vm >> k & 1u) {
             const uint32_t h = tok_hash32(t[k]);
-            const uint32_t h1 = h >> fshift, h2 = (h * 0x85EBCA6Bu) >> fshift;
-            if ((bm[h1 >> 5] >> (h1 & 31u) & 1u) && (bm[h2 >> 5] >> (h2 & 31u) & 1u)) pm |= 1u << k;
+            const uint32_t m = fmask(h);
+            if ((bm[h >> wshift] & m) == m) pm |= 1u << k;
           }
         // every valid position starts "unmatched" at order 1 (the exact match below
         // marks the matched ones)
