@@ -49,8 +49,6 @@ def main():
     cand, refs = batch(rng, 64, 128, 500, 1, dev=d)
     tb.compute_stats(cand, refs, tb.BleuConfig())
     rows = rng.integers(0, 5, (300, 3))
-    u, inv = tb.build_dictionary(*[tb.extract_ngrams(tb.TokenBatch(ids=rows[:, :2], lengths=np.full(300, 2)), 2)] * 2) \
-        if False else (None, None)
     from paper_2510_05485_b200 import _backend
     uniq, inv = _backend.unique_rows(rows)
     counts = _backend.segment_bincount(inv, np.array([100, 100, 100]), uniq.shape[0])
