@@ -87,11 +87,12 @@ size_t tb_bleu_workspace_bytes(int64_t batch, int32_t num_refs,
  * `score_corpus_from_stats` (bleu.py:293-305).
  *
  * One launch.  Per sentence group (candidate i and its R references) a CTA
- * stages the valid tokens in shared memory with bulk-async (TMA) copies,
- * builds a per-group n-gram dictionary (open-addressing hash table keyed by
- * token position, exact token comparison), counts reference n-grams with
- * warp-aggregated shared-memory atomics, max-folds over references, counts
- * the candidate with min-clipping, and runs the epilogue.
+ * stages the rows in shared memory with bulk-async (TMA) copies, builds a
+ * per-group n-gram dictionary in shared memory (a Bloom filter + exact
+ * matching of the survivors for unrelated text, a store-then-verify hash
+ * table with exact key comparison otherwise), counts the reference n-grams
+ * per reference, max-folds over references, min-clips the candidate counts,
+ * and runs the fp64 epilogue.
  *
  *  cand_ids       device (B, cand_ld) int32|int64
  *  cand_len       device (B,) int64

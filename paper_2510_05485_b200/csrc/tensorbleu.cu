@@ -11,26 +11,31 @@
 //   eff. ref   pkg/src/batchbleu/bleu.py:108-114
 //   epilogue   pkg/src/batchbleu/bleu.py:213-261, 274-305
 //
-// Design (one sentence group = candidate i + its R references):
-//   * one CTA owns a group at a time (grid-stride over groups, all CTAs resident);
-//   * the group's valid tokens are staged in shared memory with bulk-async copies
-//     (cp.async.bulk -> UBLKCP, completion on an mbarrier) while the CTA clears its
-//     hash table;
-//   * per order n, reference n-grams are inserted into an open-addressing table
-//     keyed by their smem position; equality is an exact token compare, so the
-//     dictionary is collision-free whatever the vocabulary or key width;
-//   * counts live in one 32-bit word per slot: high half = max-over-references
-//     count, low half = running count.  Warp-aggregated (match.any) shared
-//     atomics make hot keys (Zipf, vocab = 1) cost one atomic per warp;
-//   * the candidate pass adds to the low half; the returned old word gives both
-//     the running candidate count and the reference maximum, so min-clipping is
-//     fused into the same atomic (Σ min(cand, refmax) without a second sweep);
-//   * thread 0 finishes the group: effective reference length, smoothing, BP,
-//     weighted geometric mean, in fp64 with numpy's operation order.
+// Design (one sentence group = candidate i + its R references; DESIGN.md §3):
+//   * one CTA owns a group at a time (grid-stride over groups, all CTAs
+//     resident, programmatic dependent launch hides the launch gap);
+//   * the group's rows are staged in shared memory with bulk-async copies
+//     (cp.async.bulk -> UBLKCP, completion on an mbarrier) — only the valid
+//     prefixes when the rows come over PCIe from pinned host memory;
+//   * bleu_pair_kernel (R = 1): an order-1 Bloom filter drops the tokens absent
+//     from the other side; the few survivors of unrelated text are matched
+//     exactly with match.any (or by direct comparison), otherwise candidate
+//     tokens are inserted store-then-verify into a shared-memory table (plain
+//     stores, retry rounds with fresh hashes for the rare collisions) and
+//     reference tokens look up; min(cand, ref) is added once per key by its
+//     owner;
+//   * orders >= 2 visit only n-grams whose (n-1)-prefix and last token matched:
+//     key = (slot of the prefix, slot of the last token); <= 32 live positions
+//     finish in one warp with match.any, more use the same table per order;
+//   * bleu_multi_kernel (2 <= R <= 8): the same passes with one count per
+//     (reference, candidate owner), clip = min(cand, max_r ref_r);
+//     bleu_group_kernel (R > 8) walks the references one by one;
+//   * warp 0 finishes the group: effective reference length, smoothing, BP,
+//     weighted geometric mean, in fp64 with numpy's operation order;
 //   * corpus mode accumulates the int64 totals per CTA and the last CTA to
 //     finish runs the corpus epilogue (one launch in total).
-// Rows too wide for shared memory run the same code with the table and tokens
-// in global memory (64-bit count words).
+// Rows too wide for shared memory run bleu_stats_kernel with the table and
+// tokens in global memory (64-bit count words).
 
 #include "../../include/tensorbleu.h"
 
