@@ -277,13 +277,16 @@ def run_ours(args):
     # multi-rank logic can be exercised on a one-GPU box; never used for numbers
     shared = os.environ.get("TB_BENCH_SHARED_GPU") == "1"
     gpu = 0 if shared else local
-    if world > 1:
+    # TB_BENCH_FORCE_DIST=1 (testing only): the process group and its collectives
+    # even at world size 1, so the NCCL code path runs on a one-GPU box
+    distributed = world > 1 or os.environ.get("TB_BENCH_FORCE_DIST") == "1"
+    if distributed:
         torch.cuda.set_device(gpu)
         if shared:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
-    dev = torch.device("cuda", gpu if world > 1 else 0)
+    dev = torch.device("cuda", gpu if distributed else 0)
     torch.cuda.set_device(dev)
 
     b, l, v, r, smoothing = WORKLOADS[args.workload]
@@ -330,15 +333,15 @@ def run_ours(args):
         ranks, then the NCCL all-reduce of the 2N+2 int64 totals over NVLink
         and the corpus epilogue on every rank."""
         pl.run()
-        if corpus and world > 1:
+        if corpus and distributed:
             dist.all_reduce(pl.totals, op=dist.ReduceOp.SUM)
             pl.corpus_from_totals()
 
-    kernels_per_step = 1 + (1 if corpus and world > 1 else 0)
+    kernels_per_step = 1 + (1 if corpus and distributed else 0)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     # correctness gate before timing (bench.py:104-113 analogue): counts vs oracle on a slice
@@ -375,7 +378,7 @@ def run_ours(args):
         barrier()
     t_local = t_start.elapsed_time(t_end) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     value = b * world * args.steps / t_max
@@ -395,7 +398,7 @@ def run_ours(args):
     def eager_call():
         if not corpus:
             return tb.sentence_bleu(cand, refs, cfg)
-        if world == 1:
+        if not distributed:
             return tb.corpus_bleu(cand, refs, cfg)
         from paper_2510_05485_b200.distributed import allreduce_totals
         return tb.score_corpus_from_totals(allreduce_totals(tb.corpus_totals(cand, refs, cfg)), cfg)
@@ -433,7 +436,7 @@ def run_ours(args):
             """The user's call on host buffers; results come back as numpy / floats."""
             if not corpus:
                 return tb.sentence_bleu(hcand, hrefs, cfg)
-            if world == 1:
+            if not distributed:
                 return tb.corpus_bleu(hcand, hrefs, cfg)
             tot = torch.from_numpy(tb.corpus_totals(hcand, hrefs, cfg)).to(dev)  # this rank's shard
             dist.all_reduce(tot, op=dist.ReduceOp.SUM)                            # NCCL, 80 B
@@ -451,7 +454,7 @@ def run_ours(args):
             e2e_times.append(time.perf_counter() - t0)
         assert corpus or res.scores.shape == (b,)
         te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device=dev)
-        if world > 1:
+        if distributed:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         return b * world * args.steps / float(te.item()), h2d
 
@@ -497,7 +500,7 @@ def run_ours(args):
                        "global_batch": b * world, "seq_len": l, "parallelism": f"dp{world} (row shards)",
                        "timed_path": "SentenceBleuPlan.run(): one tb_bleu_stats launch per step (native binding)"
                                      + (", then NCCL all_reduce of the int64 totals + corpus epilogue kernel"
-                                        if corpus and world > 1 else "")
+                                        if corpus and distributed else "")
                                      + "; K steps back to back between two CUDA events",
                        "l2": f"inputs larger than L2: steps cycle through {nbuf} distinct device-resident "
                              f"batches ({nbuf * batch_bytes / 2**20:.0f} MiB > {l2_bytes / 2**20:.0f} MiB L2); "
@@ -514,7 +517,7 @@ def run_ours(args):
                     "int64_tokens": {"value": e2e64_value, "h2d_bytes_per_step": int(h2d64)},
                     "path": f"{'corpus' if corpus else 'sentence'}_bleu(TokenBatch(pinned host tensors)) "
                             "-> numpy: one blocking tb_bleu_host call; the kernel streams valid row prefixes "
-                            "over PCIe" + (" (+ NCCL all_reduce of the totals)" if corpus and world > 1 else "")},
+                            "over PCIe" + (" (+ NCCL all_reduce of the totals)" if corpus and distributed else "")},
             "eager_api": {"value": b * world / (np.mean(eager) / 1e3), "unit": "sentences/s",
                           "ms_per_step": float(np.mean(eager)),
                           "path": "public API on TokenBatch(CUDA tensors), eager, per-call allocation"},
@@ -526,7 +529,7 @@ def run_ours(args):
                                       "timed by its own CUDA events (includes launch latency)"},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
     return 0
