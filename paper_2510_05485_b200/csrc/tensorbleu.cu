@@ -56,6 +56,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMultiMaxRefs = 8;  // references handled by the multi-reference kernel
 constexpr int kSmallSet = 128;    // positions matched without a table (<= kThreads)
+constexpr int kMultiThreads = 384;  // multi-reference kernel: 12 warps, 2 CTAs per SM
 constexpr int kAccCopies = 32;         // replicated corpus accumulators (spread L2 atomics)
 constexpr int kGlobalKeyShift = 26;    // global-mode key = (ref << 26) | position
 constexpr uint32_t kFull = 0xffffffffu;
@@ -1290,13 +1291,13 @@ __device__ __forceinline__ void pair_retry_store(uint16_t* own, uint32_t h, int 
 // done the store half of round 1 (in its home-slot verify pass) and a barrier
 // (with first_round > 1, rounds before it are complete and the store half of
 // first_round is done).  `ids[pos]` receives the final slot.  All threads call it.
-template <typename HashF, typename EqF>
+template <int NT = kThreads, typename HashF, typename EqF>
 __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, uint16_t* lost, int nl, uint16_t* ids,
                                                   uint32_t mask, uint32_t hshift, int roff, int tid, HashF hash,
                                                   EqF eq, int first_round = 1) {
   for (int r = first_round; r <= kRetryRounds; ++r) {
     int left = 0;
-    for (int i = tid; i < nl; i += kThreads) {
+    for (int i = tid; i < nl; i += NT) {
       const uint16_t pos = lost[i];
       if (pos == 0xffffu) continue;
       const uint32_t h = hash(pos);
@@ -1313,7 +1314,7 @@ __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, 
     }
     if (!__syncthreads_or(left)) return;
   }
-  for (int i = tid; i < nl; i += kThreads) {
+  for (int i = tid; i < nl; i += NT) {
     const uint16_t pos = lost[i];
     if (pos == 0xffffu) continue;
     ids[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, ids[pos], mask, pos, pos < roff ? 1u : (1u << 16),
@@ -1957,8 +1958,9 @@ __global__ void __launch_bounds__(kThreads, 4)
 // --------------------------------------------------------------------------
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kMultiThreads, 2)
     bleu_multi_kernel(const __grid_constant__ StatsParams p) {
+  constexpr int NT = kMultiThreads;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned int s_hits[TB_MAX_ORDER];
   __shared__ int64_t s_len[kMultiMaxRefs + 1];
@@ -2025,7 +2027,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       s_len[tid] = l;
     }
     if (tid < N) s_hits[tid] = 0;
-    copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
+    copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, NT);  // tails / unaligned rows
     mbar_wait(mbar, phase);
     phase ^= 1;
     __syncthreads();
@@ -2108,15 +2110,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         return m;
       };
       // table, candidate counts and per-reference counts start empty
-      for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
-      for (int i = tid; i < (R * cpad + 7) / 8; i += kThreads) reinterpret_cast<uint4*>(rc)[i] = make_uint4(0, 0, 0, 0);
+      for (uint32_t s = tid; s < cap / 8; s += NT) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      for (int i = tid; i < (R * cpad + 7) / 8; i += NT) reinterpret_cast<uint4*>(rc)[i] = make_uint4(0, 0, 0, 0);
       if (tid == 0) {
         s_nlost = 0;
         s_ndef = 0;
         s_nsurv = 0;
       }
       __syncthreads();
-      for (int qi = tid; qi < ncq; qi += kThreads) {  // claims (plain stores)
+      for (int qi = tid; qi < ncq; qi += NT) {  // claims (plain stores)
         const int p0 = 4 * qi;
         K k[4];
         load_keys(p0, k);
@@ -2128,7 +2130,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       __syncthreads();
       if (n == 1) TB_MARK(28);
-      for (int qi = tid; qi < ncq; qi += kThreads) {  // verify
+      for (int qi = tid; qi < ncq; qi += NT) {  // verify
         const int p0 = 4 * qi;
         K k[4];
         load_keys(p0, k);
@@ -2158,7 +2160,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         *reinterpret_cast<uint2*>(ids + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
         for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
       }
-      if (order1 && tid == kThreads - 32) {  // lengths only: the last warp, off the epilogue's critical path
+      if (order1 && tid == NT - 32) {  // lengths only: the last warp, off the epilogue's critical path
         const int64_t r = closest_ref_len(s_len[0], &s_len[1], R);
         s_effref = r;
         s_bp = brevity_penalty_fp64(s_len[0], r);
@@ -2169,7 +2171,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       auto hashk = [&](uint16_t q) { return tok_hash32(keys[q]); };
       auto eqk = [&](uint16_t a, uint16_t c) { return keys[a] == keys[c]; };
       int left = 0;
-      for (int i = tid; i < nl; i += kThreads) {  // retry round 1 (verify half) ...
+      for (int i = tid; i < nl; i += NT) {  // retry round 1 (verify half) ...
         const uint16_t pos = lost[i];
         const uint32_t h = hashk(pos);
         const uint32_t cs = rehash(h, 1, hshift);
@@ -2183,7 +2185,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           pair_retry_store(own, h, 2, hshift, pos);
         }
       }
-      for (int qi = tid; qi < nrq; qi += kThreads) {  // ... with the home-slot lookups of all references
+      for (int qi = tid; qi < nrq; qi += NT) {  // ... with the home-slot lookups of all references
         int r, p0;
         const uint32_t vm0 = ref_quad(qi, r, p0);
         K k[4];
@@ -2217,10 +2219,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (ids2) *reinterpret_cast<uint2*>(ids2 + p0) = vv;
       }
       if (__syncthreads_or(left))
-        pair_resolve_lost(own, cnt, lost, nl, ids, mask, hshift, cpad, tid, hashk, eqk, 2);
+        pair_resolve_lost<NT>(own, cnt, lost, nl, ids, mask, hshift, cpad, tid, hashk, eqk, 2);
       if (n == 1) TB_MARK(3);
       const int nd = s_ndef;
-      for (int i = tid; i < nd; i += kThreads) {  // deferred lookups: the full chain
+      for (int i = tid; i < nd; i += NT) {  // deferred lookups: the full chain
         const uint16_t pos = defl[i];
         const K key = keys[pos];
         uint16_t o;
@@ -2236,7 +2238,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncthreads();
       if (n == 1) TB_MARK(26);
       unsigned int hits = 0;
-      for (int qi = tid; qi < ncq; qi += kThreads) {  // candidate liveness + clipped count
+      for (int qi = tid; qi < ncq; qi += NT) {  // candidate liveness + clipped count
         const int p0 = 4 * qi;
         K k[4];
         load_keys(p0, k);
@@ -2281,7 +2283,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (; n <= N && nsurv > kSmallSet; ++n) {
       // packed keys of the positions whose (n-1)-prefix and last token are live
       const int nq_all = ncq + nrq;
-      for (int qi = tid; qi < nq_all; qi += kThreads) {
+      for (int qi = tid; qi < nq_all; qi += NT) {
         int r = 0, p0 = 4 * qi;
         const uint32_t vm = qi < ncq ? cand_mask(p0) : ref_quad(qi - ncq, r, p0);
         const int end = row_end(p0);
@@ -2722,7 +2724,7 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
 
 template <typename K>
 int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool persistent_fill,
-                  size_t* attr_set, cudaStream_t stream) {
+                  size_t* attr_set, cudaStream_t stream, int threads = kThreads) {
   int dev = 0;
   TB_CUDA(cudaGetDevice(&dev));
   if (pl.smem_bytes > 48 * 1024 && attr_set[dev & 63] < pl.smem_bytes) {
@@ -2740,7 +2742,7 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
     for (auto& e : cache)
       if (e.occ > 0 && e.dev == dev && e.smem == pl.smem_bytes) occ = e.occ;
     if (occ == 0) {
-      TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, pl.smem_bytes));
+      TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, pl.smem_bytes));
       if (occ < 1) occ = 1;
       cache[next] = {dev, pl.smem_bytes, occ};
       next = (next + 1) & 7;
@@ -2750,7 +2752,7 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = pl.smem_bytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -2771,7 +2773,7 @@ int launch_stats(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t s
   }
   if (pl.multi) {
     static size_t attr_set[64] = {0};
-    return launch_kernel(bleu_multi_kernel<T>, prm, pl, sms, true, attr_set, stream);
+    return launch_kernel(bleu_multi_kernel<T>, prm, pl, sms, true, attr_set, stream, kMultiThreads);
   }
   if (pl.smem_mode) {
     static size_t attr_set[64] = {0};
