@@ -56,7 +56,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMultiMaxRefs = 8;  // references handled by the multi-reference kernel
 constexpr int kSmallSet = 128;    // positions matched without a table (<= kThreads)
-constexpr int kMultiThreads = 384;  // multi-reference kernel: 12 warps, 2 CTAs per SM
+constexpr int kMultiThreads = 512;  // multi-reference kernel: 16 warps, 2 CTAs per SM
 constexpr int kAccCopies = 32;         // replicated corpus accumulators (spread L2 atomics)
 constexpr int kGlobalKeyShift = 26;    // global-mode key = (ref << 26) | position
 constexpr uint32_t kFull = 0xffffffffu;
