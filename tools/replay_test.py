@@ -1,6 +1,7 @@
+"""Graph replay vs direct launches of the c2 step (GPU box): why bench.py times
+plan.run() — replaying 64 alternating one-kernel CUDA graphs costs extra GPU
+time per step at large step counts (profiles/r01_experiments.md)."""
 import sys, time, torch
-sys.path.insert(0, '/root/repo')
-import bench, paper_2510_05485_b200 as tb
 b, l, v, r, sm = bench.WORKLOADS["c2"]
 dev = torch.device("cuda", 0)
 plans = []
