@@ -2,6 +2,8 @@
 plan.run() — replaying 64 alternating one-kernel CUDA graphs costs extra GPU
 time per step at large step counts (profiles/r01_experiments.md)."""
 import sys, time, torch
+sys.path.insert(0, '/root/repo')
+import bench, paper_2510_05485_b200 as tb
 b, l, v, r, sm = bench.WORKLOADS["c2"]
 dev = torch.device("cuda", 0)
 plans = []
