@@ -509,8 +509,13 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": a_bytes,
+                         # the DRAM bytes the kernel really moves (ncu) over the same step time:
+                         # how far from HBM-bound it is (it is latency-bound)
+                         "dram_achieved": (traffic / kernel_s / 1e9) if traffic else None,
+                         "dram_frac": (traffic / kernel_s / 1e9 / peak) if traffic else None,
                          "note": "A = SURVEY §8(d) paper-dataflow bytes; the fused kernel only reads the "
-                                 f"{input_bytes} B of int32 tokens, so frac > 1 means it beats the paper dataflow"},
+                                 f"{input_bytes} B of int32 tokens, so frac > 1 means it beats the paper dataflow; "
+                                 "dram_frac = ncu DRAM bytes per launch / step time / peak"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "sentences/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "token_dtype": "int32",
