@@ -393,3 +393,31 @@ def test_apply_smoothing_reference_examples():
     assert p[0, 0] == 0.0 and p[0, 1] == pytest.approx(0.25)
     for m in SMOOTHINGS:
         assert tb.apply_smoothing(stats([[0]], [[0]]), tb.BleuConfig(max_order=1, smoothing=m))[0, 0] == 0.0
+
+
+def test_filter_path_boundaries_and_mixed_regimes():
+    """Rows whose candidate and reference share exactly K tokens, so that the
+    order-1 filter keeps ~2K positions: around the warp (32) and block (128)
+    limits of the exact-match paths and beyond (hash passes); > 592 rows so
+    CTAs process several groups and switch regimes mid-launch."""
+    rng = np.random.default_rng(33)
+    L = 300
+    ks = [0, 1, 15, 16, 17, 31, 32, 33, 63, 64, 65, 100, 150]
+    rows_c, rows_r, lc, lr = [], [], [], []
+    for i in range(700):
+        k = ks[i % len(ks)]
+        shared = rng.choice(1000, size=k, replace=False) + 10_000
+        cand = np.concatenate([shared, rng.integers(100_000, 200_000, L - k)])
+        ref = np.concatenate([rng.permutation(shared), rng.integers(300_000, 400_000, L - k)])
+        if i % 3 == 0:  # repeats of shared tokens on both sides
+            cand[-5:] = shared[:5] if k >= 5 else cand[-5:]
+        rng.shuffle(cand)
+        rng.shuffle(ref)
+        rows_c.append(cand)
+        rows_r.append(ref)
+        lc.append(int(rng.integers(L - 20, L + 1)))
+        lr.append(int(rng.integers(L - 20, L + 1)))
+    cid, rid = np.stack(rows_c), np.stack(rows_r)
+    clen, rlen = np.array(lc), np.array(lr)
+    for dtype in (torch.int32, torch.int64):
+        _check_against_oracle(cid, clen, [(rid, rlen)], tb.BleuConfig(smoothing="floor"), dtype=dtype)
