@@ -54,6 +54,7 @@
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kPairCtasPerSm = 4;  // single-reference kernel: 4 CTAs of kThreads per SM
 constexpr int kMultiMaxRefs = 8;  // references handled by the multi-reference kernel
 constexpr int kSmallSet = 128;    // positions matched without a table (<= kThreads)
 constexpr int kMultiThreads = 512;  // multi-reference kernel: 16 warps, 2 CTAs per SM
@@ -120,6 +121,7 @@ struct StatsParams {
   int ref_off[TB_MAX_REFS + 1];
   // pruned shared-memory kernel: byte offsets of the per-position / table arrays
   int off_id1, off_idn, off_live, off_ent, off_mref, off_kc, off_lists, off_seg;
+  int off_tok2;  // pair kernel: second token buffer (prefetch of the next group), 0 = none
   // global-memory mode
   unsigned char* gtab;
   size_t gtab_stride;
@@ -1377,9 +1379,12 @@ __global__ void __launch_bounds__(kThreads, 4)
   const int cpad = p.cand_pad;
   const int roff = cpad;  // first reference position (multiple of 4)
 
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
-  T* tok = reinterpret_cast<T*>(smem + 16);
-  uint32_t* kc = reinterpret_cast<uint32_t*>(smem + 16);           // aliases tok (orders >= 2)
+  uint64_t* mbars = reinterpret_cast<uint64_t*>(smem);  // one mbarrier per token buffer
+  T* const tokb[2] = {reinterpret_cast<T*>(smem + 16), reinterpret_cast<T*>(smem + p.off_tok2)};
+  const bool dbuf = p.off_tok2 != 0;  // prefetch the next group into the other buffer
+  int cur = 0;
+  T* tok = tokb[0];
+  uint32_t* kc = reinterpret_cast<uint32_t*>(tok);                 // aliases tok (orders >= 2)
   uint16_t* id1 = reinterpret_cast<uint16_t*>(smem + p.off_id1);   // order-1 slot; 0xffff: token unmatched
   uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot; 0xffff: n-gram unmatched
   uint16_t* own = reinterpret_cast<uint16_t*>(smem + p.off_ent);   // slot -> owner position, 0xffff = empty
@@ -1388,23 +1393,26 @@ __global__ void __launch_bounds__(kThreads, 4)
   const uint32_t hshift = 32 - cap_log2;
   const uint32_t mask = cap - 1;
 
-  auto issue_stage = [&](int64_t b) {
-    if (tid == 0) issue_rows<T>(p, b, 2, tok, mbar, s_stage_len, &s_flags);
+  auto issue_stage = [&](int64_t b, int buf) {
+    if (tid == 0) issue_rows<T>(p, b, 2, tokb[buf], mbars + buf, s_stage_len, &s_flags);
   };
 
   if (tid < 2 * N + 2) s_tot[tid] = 0;
   if (tid == 0) {
     s_flags = 0;
-    mbar_init(mbar, 1);
+    mbar_init(mbars, 1);
+    if (dbuf) mbar_init(mbars + 1, 1);
   }
   griddep_wait_and_release();
-  if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
+  if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x, 0);
   __syncthreads();
   TB_MARK(0);
-  uint32_t phase = 0;
+  uint32_t phases = 0;  // bit i: parity of mbarrier i
   bool try_filter = true;  // off after a group of this CTA needed the hash passes (related text)
 
   for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    tok = tokb[cur];
+    kc = reinterpret_cast<uint32_t*>(tok);
     if (p.prefix_only) {
       __syncthreads();  // s_stage_len of this group, written by thread 0 in issue_rows
       if (tid < 2) s_len[tid] = s_stage_len[tid];
@@ -1431,9 +1439,11 @@ __global__ void __launch_bounds__(kThreads, 4)
       const uint32_t fill = try_filter ? 0u : ~0u;
       for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(fill, fill, fill, fill);
     }
-    mbar_wait(mbar, phase);
-    phase ^= 1;
+    mbar_wait(mbars + cur, (phases >> cur) & 1u);
+    phases ^= 1u << cur;
     __syncthreads();
+    // every thread is past the previous group: its buffer takes the next group
+    if (dbuf && b + gridDim.x < p.batch) issue_stage(b + gridDim.x, cur ^ 1);
     TB_MARK(2);
 
     const int clen = static_cast<int>(s_len[0]);
@@ -1932,9 +1942,13 @@ __global__ void __launch_bounds__(kThreads, 4)
         }
       }
     }
-    if (b + gridDim.x < p.batch) {
+    if (!dbuf && b + gridDim.x < p.batch) {
       __syncthreads();
-      issue_stage(b + gridDim.x);
+      issue_stage(b + gridDim.x, 0);
+    }
+    if (dbuf) {
+      cur ^= 1;
+      __syncthreads();  // s_len / s_hits of this group are read before the next group resets them
     }
     TB_MARK(30);
   }
@@ -2519,6 +2533,7 @@ struct Plan {
   int cand_pad = 0;
   int ref_off[TB_MAX_REFS + 1] = {0};
   int off_id1 = 0, off_idn = 0, off_live = 0, off_ent = 0, off_mref = 0, off_kc = 0, off_lists = 0, off_seg = 0;
+  int off_tok2 = 0;
   size_t smem_bytes = 0;   // dynamic smem (smem mode)
   size_t gtab_stride = 0;  // per-CTA table bytes (global mode)
   int64_t grid = 0;
@@ -2576,7 +2591,8 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
     int lg = cap_log2_for(4 * ptot, 6);
     int64_t offs[6];
     int64_t total = pair_layout(lg, offs);
-    while (total + static_cast<int64_t>(kStaticSmemReserve) > smem_optin / 4 && (int64_t(1) << (lg - 1)) >= 2 * ptot) {
+    while (total + static_cast<int64_t>(kStaticSmemReserve) > smem_optin / kPairCtasPerSm &&
+           (int64_t(1) << (lg - 1)) >= 2 * ptot) {
       --lg;
       total = pair_layout(lg, offs);
     }
@@ -2593,6 +2609,15 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       pl->off_mref = static_cast<int>(offs[3]);
       pl->off_lists = static_cast<int>(offs[4]);
       pl->smem_bytes = static_cast<size_t>(total);
+      // CTAs that process several groups prefetch the next group's rows into a
+      // second token buffer while they work on the current one — when that
+      // buffer still fits kPairCtasPerSm CTAs per SM
+      const int64_t tok2 = round_up(ptot * (token_bytes > 4 ? token_bytes : 4), 16);
+      if (batch > static_cast<int64_t>(kPairCtasPerSm) * sms &&
+          total + tok2 + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin / kPairCtasPerSm) {
+        pl->off_tok2 = static_cast<int>(total);
+        pl->smem_bytes = static_cast<size_t>(total + tok2);
+      }
       pl->ws_bytes = pl->acc_bytes;
       return TB_OK;
     }
@@ -2887,6 +2912,7 @@ static int stats_impl(int32_t token_bytes, const void* cand_ids, int64_t cand_ld
   prm.off_kc = pl.off_kc;
   prm.off_lists = pl.off_lists;
   prm.off_seg = pl.off_seg;
+  prm.off_tok2 = pl.off_tok2;
   prm.gtab = pl.smem_mode ? nullptr : ws + pl.acc_bytes;
   prm.gtab_stride = pl.gtab_stride;
   prm.prefix_only = prefix_only && pl.smem_mode;
