@@ -116,6 +116,7 @@ struct StatsParams {
   int32_t* err;             // written by the last CTA
   // hash table
   int cap_log2;
+  int filter_log2;  // pair kernel: 32-bit words per side of the order-1 filter (log2)
   // shared-memory layout (elements of the token type)
   int cand_pad;
   int ref_off[TB_MAX_REFS + 1];
@@ -1325,6 +1326,76 @@ __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, 
   __syncthreads();
 }
 
+// pair_resolve_lost for the live-list passes of orders >= 2: `lost` holds list
+// indices e (owners are list indices, keys kc[e], hash key * 0x9E3779B1), all of
+// candidate entries; settling e writes its owner's list index to idn[lin[e]].
+template <int NT = kThreads>
+__device__ __forceinline__ void list_resolve_lost(uint16_t* own, uint32_t* cnt, const uint32_t* kc, uint16_t* lost,
+                                                  int nl, const uint16_t* lin, uint16_t* idn, uint32_t mask,
+                                                  uint32_t hshift, int tid) {
+  for (int r = 1; r <= kRetryRounds; ++r) {
+    int left = 0;
+    for (int i = tid; i < nl; i += NT) {
+      const uint16_t e = lost[i];
+      if (e == 0xffffu) continue;
+      const uint32_t key = kc[e];
+      const uint32_t h = key * 0x9E3779B1u;
+      const uint16_t w = own[rehash(h, r, hshift)];
+      if (w == e || kc[w] == key) {
+        if (w != e) atomicAdd(&cnt[w], 1u);
+        idn[lin[e]] = w;
+        lost[i] = 0xffffu;
+      } else {
+        left = 1;
+        if (r < kRetryRounds) pair_retry_store(own, h, r + 1, hshift, e);
+      }
+    }
+    if (!__syncthreads_or(left)) return;
+  }
+  for (int i = tid; i < nl; i += NT) {
+    const uint16_t e = lost[i];
+    if (e == 0xffffu) continue;
+    const uint32_t key = kc[e];
+    const uint32_t sl = pair_insert_loser(own, cnt, (key * 0x9E3779B1u) >> hshift, mask, e, 1u,
+                                          [&](uint16_t x) { return kc[x] == key; });
+    uint16_t w;
+    asm volatile("ld.volatile.shared.u16 %0, [%1];" : "=h"(w) : "r"(smem_u32(own) + 2 * sl));
+    idn[lin[e]] = w;
+  }
+  __syncthreads();
+}
+
+// Warp-aggregated appends to a shared list (one atomic per warp).  All 32 lanes
+// call.  warp_append: one value per lane.
+__device__ __forceinline__ void warp_append(uint16_t* list, int* count, bool want, int v, int lane) {
+  const unsigned m = __ballot_sync(kFull, want);
+  if (!m) return;
+  const int src = __ffs(m) - 1;
+  int base = 0;
+  if (lane == src) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(kFull, base, src);
+  if (want) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(v);
+}
+// warp_append_quad: the values v(k) for the set bits k of m (4 bits per lane),
+// offsets by a warp prefix sum of the per-lane counts
+template <typename V>
+__device__ __forceinline__ void warp_append_quad(uint16_t* list, int* count, uint32_t m, V v, int lane) {
+  if (!__any_sync(kFull, m != 0)) return;
+  const int n = __popc(m);
+  int incl = n;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  int base = 0;
+  if (lane == 31) base = atomicAdd(count, incl);
+  base = __shfl_sync(kFull, base, 31) + incl - n;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (m >> k & 1u) list[base++] = static_cast<uint16_t>(v(k));
+}
+
 // Slot of token t among the inserted (candidate) tokens, or -1; *owner gets its
 // owner position.  Follows an inserted key's placement order: home slot, the
 // retry rounds' slots, then linear probing from home + 1 — a key sits at the
@@ -1364,9 +1435,8 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ int64_t s_len[2];
   __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
   __shared__ int s_last, s_flags;
-  __shared__ int s_nlost, s_nsurv, s_ndef, s_nf;
+  __shared__ int s_nlost, s_nc, s_nr, s_ndef, s_nf;  // s_nc / s_nr: live candidate / reference entries
   __shared__ uint16_t s_flist[kSmallSet];  // positions that pass the order-1 filter
-  __shared__ uint16_t s_surv[kSmallSet];  // order-1 survivors (the first kSmallSet)
   __shared__ int64_t s_stage_len[2];  // prefix mode: lengths read by issue_rows
   __shared__ double s_bp;             // brevity penalty of the current group
 
@@ -1389,7 +1459,13 @@ __global__ void __launch_bounds__(kThreads, 4)
   uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot; 0xffff: n-gram unmatched
   uint16_t* own = reinterpret_cast<uint16_t*>(smem + p.off_ent);   // slot -> owner position, 0xffff = empty
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + p.off_mref);  // owner -> [ref 16 | cand 16], owner excluded
-  uint16_t* lost = reinterpret_cast<uint16_t*>(smem + p.off_lists);  // positions whose home slot holds another key
+  // two position lists of ptot entries: the live positions of an order (input of
+  // the next; candidate positions from index 0, reference positions from index
+  // roff) and, in the other, the lost (from 0) / deferred (from roff) entries of
+  // the current order.  Owners are always candidate entries: cnt has cand_pad words.
+  const int ptot = roff + p.ref_off[1];
+  uint16_t* const lx = reinterpret_cast<uint16_t*>(smem + p.off_lists);
+  uint16_t* const ly = lx + ptot;
   const uint32_t hshift = 32 - cap_log2;
   const uint32_t mask = cap - 1;
 
@@ -1429,15 +1505,20 @@ __global__ void __launch_bounds__(kThreads, 4)
     if (tid < N) s_hits[tid] = 0;
     if (tid == 0) {
       s_nlost = 0;
-      s_nsurv = 0;
+      s_nc = 0;
+      s_nr = 0;
       s_ndef = 0;
       s_nf = 0;
     }
     copy_row_tails<T>(p, b, 2, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
-    // the table region starts as the two filter bitmaps (zero) or as the empty table
-    {
-      const uint32_t fill = try_filter ? 0u : ~0u;
-      for (uint32_t s = tid; s < cap / 8; s += kThreads) reinterpret_cast<uint4*>(own)[s] = make_uint4(fill, fill, fill, fill);
+    // the table region starts as the two filter bitmaps (zero; they extend over
+    // the count array) or as the empty table
+    if (try_filter) {
+      for (uint32_t s = tid; s < (1u << p.filter_log2) / 2; s += kThreads)
+        reinterpret_cast<uint4*>(own)[s] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (uint32_t s = tid; s < cap / 8; s += kThreads)
+        reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
     }
     mbar_wait(mbars + cur, (phases >> cur) & 1u);
     phases ^= 1u << cur;
@@ -1494,8 +1575,8 @@ __global__ void __launch_bounds__(kThreads, 4)
     if (try_filter) {
       // blocked: both bits of a token in one 32-bit word (one atomic / one load)
       uint32_t* bmc = reinterpret_cast<uint32_t*>(own);  // candidate tokens
-      uint32_t* bmr = bmc + cap / 4;                      // reference tokens
-      const uint32_t wshift = hshift + 2;                 // cap / 4 words per filter
+      uint32_t* bmr = bmc + (1u << p.filter_log2);        // reference tokens
+      const uint32_t wshift = 32 - p.filter_log2;
       auto fmask = [](uint32_t h) {
         const uint32_t g = h * 0x85EBCA6Bu;
         return (1u << (g >> 27)) | (1u << ((g >> 22) & 31u));
@@ -1560,11 +1641,14 @@ __global__ void __launch_bounds__(kThreads, 4)
             id1[pos] = static_cast<uint16_t>(leader);
             idn[pos] = static_cast<uint16_t>(leader);
           }
-          const unsigned lm = __ballot_sync(kFull, live);
-          if (live) s_surv[__popc(lm & ((1u << lane) - 1u))] = static_cast<uint16_t>(pos);
+          const unsigned lc = __ballot_sync(kFull, live && pos < roff);
+          const unsigned lr = __ballot_sync(kFull, live && pos >= roff);
+          const unsigned below = (1u << lane) - 1u;
+          if (live) lx[pos < roff ? __popc(lc & below) : roff + __popc(lr & below)] = static_cast<uint16_t>(pos);
           if (lane == 0) {
             s_hits[0] = h;
-            s_nsurv = __popc(lm);
+            s_nc = __popc(lc);
+            s_nr = __popc(lr);
           }
         }
       } else if (S <= kSmallSet) {
@@ -1589,8 +1673,8 @@ __global__ void __launch_bounds__(kThreads, 4)
           if (live) {
             id1[pos] = static_cast<uint16_t>(leader);
             idn[pos] = static_cast<uint16_t>(leader);
-            const int j = atomicAdd(&s_nsurv, 1);
-            if (j < kSmallSet) s_surv[j] = static_cast<uint16_t>(pos);
+            if (pos < roff) lx[atomicAdd(&s_nc, 1)] = static_cast<uint16_t>(pos);
+            else lx[roff + atomicAdd(&s_nr, 1)] = static_cast<uint16_t>(pos);
           }
         }
       } else {  // related text: reset the table region for the hash passes
@@ -1602,7 +1686,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       TB_MARK(22);
     }
 
-    if (!filtered) {
+    if (__builtin_expect(!filtered, 0)) {  // (unlikely: keeps the filter path's code contiguous)
     // ================= order 1: tokens =================
     // Only candidate tokens are inserted (store-then-verify); reference tokens
     // look up: a reference token absent from the candidate can neither be
@@ -1649,7 +1733,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         }
       }
       *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
-      for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
+      for (; lm; lm &= lm - 1) ly[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
     }
     // the brevity penalty depends on the lengths only: the last warp (idle in the
     // candidate passes unless the candidate has > 7/8 * 4 * blockDim tokens)
@@ -1668,7 +1752,8 @@ __global__ void __launch_bounds__(kThreads, 4)
       // retry rounds have settled.  The store halves only fill EMPTY slots,
       // and a home read EMPTY here stays conclusive for that token.
       const int nl = s_nlost;
-      uint16_t* defl = lost + roff;  // deferred reference positions (capacity: padded ref width)
+      uint16_t* const lost = ly;
+      uint16_t* const defl = ly + roff;  // deferred reference positions (capacity: padded ref width)
       auto hash1 = [&](uint16_t q) { return tok_hash32(tok[q]); };
       auto eq1 = [&](uint16_t a, uint16_t b) { return tok[a] == tok[b]; };
       int left = 0;
@@ -1686,8 +1771,11 @@ __global__ void __launch_bounds__(kThreads, 4)
           pair_retry_store(own, h, 2, hshift, pos);
         }
       }
-      for (int qi = tid; qi < nrq; qi += kThreads) {  // reference lookups (home slots)
+      for (int q0 = 0; q0 < nrq; q0 += kThreads) {  // reference lookups (home slots)
+        const int qi = q0 + tid;
         const int p0 = roff + 4 * qi;
+        uint32_t fm = 0;  // found: live at order 1
+        if (qi < nrq) {
         const uint32_t vm = roff + rlen - p0 >= 4 ? 0xfu : ((1u << (roff + rlen - p0)) - 1u);
         T t[4];
         load4(p0, t);
@@ -1710,38 +1798,47 @@ __global__ void __launch_bounds__(kThreads, 4)
             v[k] = 0xffffu;
           } else {
             atomicAdd(&cnt[o[k]], 1u << 16);
-            const int j = atomicAdd(&s_nsurv, 1);  // survivors are rare on unrelated text
-            if (j < 32) s_surv[j] = static_cast<uint16_t>(p0 + k);
+            fm |= 1u << k;
           }
         }
         const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
         *reinterpret_cast<uint2*>(id1 + p0) = vv;  // 0xffff: token absent from the candidate
         *reinterpret_cast<uint2*>(idn + p0) = vv;
+        }
+        warp_append_quad(lx + roff, &s_nr, fm, [&](int k) { return p0 + k; }, lane);
       }
       if (__syncthreads_or(left))
         pair_resolve_lost(own, cnt, lost, nl, id1, mask, hshift, roff, tid, hash1, eq1, 2);
       TB_MARK(3);
       const int nd = s_ndef;
-      for (int i = tid; i < nd; i += kThreads) {  // deferred lookups: the full chain
-        const uint16_t pos = defl[i];
-        const T t = tok[pos];
-        uint16_t o;
-        const int sl = pair_find_retry(own, tok, t, tok_hash32(t), hshift, mask, &o);
-        if (sl >= 0) {
-          atomicAdd(&cnt[o], 1u << 16);
-          id1[pos] = static_cast<uint16_t>(sl);
-          idn[pos] = static_cast<uint16_t>(sl);
-          const int j = atomicAdd(&s_nsurv, 1);
-          if (j < 32) s_surv[j] = pos;
+      for (int i0 = 0; i0 < nd; i0 += kThreads) {  // deferred lookups: the full chain
+        const int i = i0 + tid;
+        bool f = false;
+        int pos = 0;
+        if (i < nd) {
+          pos = defl[i];
+          const T t = tok[pos];
+          uint16_t o;
+          const int sl = pair_find_retry(own, tok, t, tok_hash32(t), hshift, mask, &o);
+          if (sl >= 0) {
+            atomicAdd(&cnt[o], 1u << 16);
+            id1[pos] = static_cast<uint16_t>(sl);
+            idn[pos] = static_cast<uint16_t>(sl);
+            f = true;
+          }
         }
+        warp_append(lx + roff, &s_nr, f, pos, lane);
       }
     }
     __syncthreads();
     TB_MARK(26);
     {  // candidate liveness + clipped count (added once per slot by its owner)
       unsigned int hits = 0;
-      for (int qi = tid; qi < ncq; qi += kThreads) {
+      for (int q0 = 0; q0 < ncq; q0 += kThreads) {
+        const int qi = q0 + tid;
         const int p0 = 4 * qi;
+        uint32_t lm = 0;
+        if (qi < ncq) {
         const uint32_t vm = clen - p0 >= 4 ? 0xfu : ((1u << (clen - p0)) - 1u);
         const uint2 s2 = *reinterpret_cast<const uint2*>(id1 + p0);
         const uint32_t s[4] = {s2.x & 0xffffu, s2.x >> 16, s2.y & 0xffffu, s2.y >> 16};
@@ -1761,14 +1858,15 @@ __global__ void __launch_bounds__(kThreads, 4)
             if (o[k] == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
             if (x != 0) {
               v[k] = s[k];
-              const int j = atomicAdd(&s_nsurv, 1);
-              if (j < 32) s_surv[j] = static_cast<uint16_t>(pos);
+              lm |= 1u << k;
             }
           }
         }
         const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
         *reinterpret_cast<uint2*>(id1 + p0) = vv;  // 0xffff: token unmatched, no n-gram can contain it
         *reinterpret_cast<uint2*>(idn + p0) = vv;
+        }
+        warp_append_quad(lx, &s_nc, lm, [&](int k) { return p0 + k; }, lane);
       }
       hits = __reduce_add_sync(kFull, hits);
       if (lane == 0 && hits) atomicAdd(&s_hits[0], hits);
@@ -1776,17 +1874,208 @@ __global__ void __launch_bounds__(kThreads, 4)
     __syncthreads();
     }
     TB_MARK(4);
-    int nsurv = s_nsurv;
+    int nc = s_nc, nr = s_nr;
 
     // ================= orders n >= 2 =================
-    if (nsurv > 0 && nsurv <= 32 && N >= 2) {
-      // Few survivors: warp 0 finishes every remaining order with match.any on the
-      // keys (no table, no block barriers).  An n-gram's id for the next order is
-      // the lowest lane holding it.
+    // The live positions of order n-1 (list lin, nsurv entries; idn[pos]: id of
+    // pos's (n-1)-gram, canonical within that order) form the keys of order n:
+    // (idn[pos] << 16 | id1[pos + n - 1]).  While more than 32 stay live, one
+    // table pass per order over the LIST (not all positions): candidate keys
+    // claim, candidate entries verify and reference entries look up (like order
+    // 1), then the live pass adds the clipped counts, appends the survivors to
+    // the other list and clears the table for the next order.  Owners, counts
+    // and ids are list indices (kc[i], cnt[i]).  With at most 32 live, warp 0
+    // finishes the remaining orders with match.any (no table, no barriers).
+    uint16_t* lin = lx;
+    uint16_t* lout = ly;
+    int n = 2;
+    bool cleared = false;  // own[] still holds order 1's table (or the filter bitmaps)
+    while (__builtin_expect(n <= N && nc > 0 && nc + nr > 32, 0)) {
+      // entry quads: candidate entries [0, nc) then reference entries [roff, roff + nr)
+      const int mcq = (nc + 3) >> 2;
+      const int mq = mcq + ((nr + 3) >> 2);
+      auto equad = [&](int qi, int& i0) -> uint32_t {
+        int left;
+        if (qi < mcq) {
+          i0 = 4 * qi;
+          left = nc - i0;
+        } else {
+          i0 = roff + 4 * (qi - mcq);
+          left = nr - (i0 - roff);
+        }
+        return left >= 4 ? 0xfu : ((1u << left) - 1u);
+      };
+      auto lpos = [&](int i0, int (&pos)[4]) {
+        const uint2 l2 = *reinterpret_cast<const uint2*>(lin + i0);
+        pos[0] = l2.x & 0xffffu;
+        pos[1] = l2.x >> 16;
+        pos[2] = l2.y & 0xffffu;
+        pos[3] = l2.y >> 16;
+      };
+      if (!cleared)
+        for (uint32_t s = tid; s < cap / 8; s += kThreads)
+          reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      for (int qi = tid; qi < mq; qi += kThreads) {  // keys (~0: dead), counts, candidate claims
+        int i0;
+        const uint32_t vm = equad(qi, i0);
+        int pos[4];
+        lpos(i0, pos);
+        const int end = i0 < roff ? clen : roff + rlen;
+        uint32_t key[4];
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          key[k] = ~0u;
+          const int q = pos[k] + n - 1;
+          if ((vm >> k & 1u) && q < end) {
+            const uint16_t l = id1[q];
+            if (l != 0xffffu) key[k] = (static_cast<uint32_t>(idn[pos[k]]) << 16) | l;
+          }
+        }
+        *reinterpret_cast<uint4*>(kc + i0) = make_uint4(key[0], key[1], key[2], key[3]);
+        if (i0 < roff) {
+          *reinterpret_cast<uint4*>(cnt + i0) = make_uint4(0, 0, 0, 0);
+          if (cleared) {
+  #pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (key[k] != ~0u) own[(key[k] * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(i0 + k);
+          }
+        }
+      }
+      if (tid == 0) {
+        s_nlost = 0;
+        s_ndef = 0;
+      }
+      __syncthreads();
+      if (!cleared) {
+        for (int qi = tid; qi < mcq; qi += kThreads) {
+          const int i0 = 4 * qi;
+          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + i0);
+          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+  #pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (key[k] != ~0u) own[(key[k] * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(i0 + k);
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {  // every thread has read them (barrier above)
+        s_nc = 0;
+        s_nr = 0;
+      }
+      uint16_t* const defl = lout + roff;  // deferred reference entries (lost candidates from 0)
+      for (int qi = tid; qi < mq; qi += kThreads) {  // verify (candidates) / home lookups (references)
+        int i0;
+        equad(qi, i0);
+        int pos[4];
+        lpos(i0, pos);
+        const uint4 k4 = *reinterpret_cast<const uint4*>(kc + i0);
+        const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+        uint16_t w[4];
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = key[k] != ~0u ? own[(key[k] * 0x9E3779B1u) >> hshift] : 0xffffu;
+        uint32_t kw[4];
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) kw[k] = w[k] != 0xffffu ? kc[w[k]] : ~0u;
+        if (i0 < roff) {
+  #pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (key[k] == ~0u) continue;
+            const int i = i0 + k;
+            if (w[k] == i) {
+              idn[pos[k]] = static_cast<uint16_t>(i);
+            } else if (kw[k] == key[k]) {
+              atomicAdd(&cnt[w[k]], 1u);
+              idn[pos[k]] = w[k];
+            } else {
+              lout[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(i);
+              pair_retry_store(own, key[k] * 0x9E3779B1u, 1, hshift, static_cast<uint16_t>(i));
+            }
+          }
+        } else {
+  #pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (key[k] == ~0u) continue;
+            const int i = i0 + k;
+            if (w[k] == 0xffffu) {  // empty home: no candidate n-gram has this key
+              kc[i] = ~0u;
+            } else if (kw[k] == key[k]) {
+              atomicAdd(&cnt[w[k]], 1u << 16);
+              idn[pos[k]] = w[k];
+            } else {
+              defl[atomicAdd(&s_ndef, 1)] = static_cast<uint16_t>(i);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (s_nlost) list_resolve_lost(own, cnt, kc, lout, s_nlost, lin, idn, mask, hshift, tid);
+      if (s_ndef) {
+        const int nd = s_ndef;
+        for (int j = tid; j < nd; j += kThreads) {
+          const uint16_t i = defl[j];
+          const uint32_t key = kc[i];
+          uint16_t w;
+          if (pair_find_retry(own, kc, key, key * 0x9E3779B1u, hshift, mask, &w) >= 0) {
+            atomicAdd(&cnt[w], 1u << 16);
+            idn[lin[i]] = w;
+          } else {
+            kc[i] = ~0u;
+          }
+        }
+        __syncthreads();
+      }
+      // live: clipped counts (owners), survivors to lout, the table cleared
+      if (n < N)
+        for (uint32_t s = tid; s < cap / 8; s += kThreads)
+          reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      unsigned int hits = 0;
+      for (int q0 = 0; q0 < mq; q0 += kThreads) {
+        const int qi = q0 + tid;
+        int i0 = 0;
+        uint32_t lm = 0;
+        int pos[4] = {0, 0, 0, 0};
+        if (qi < mq) {
+          equad(qi, i0);
+          lpos(i0, pos);
+          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + i0);
+          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+          uint32_t w[4], cw[4];
+  #pragma unroll
+          for (int k = 0; k < 4; ++k) w[k] = key[k] != ~0u ? idn[pos[k]] : 0u;
+  #pragma unroll
+          for (int k = 0; k < 4; ++k) cw[k] = key[k] != ~0u ? cnt[w[k]] : 0u;
+  #pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (key[k] == ~0u) continue;
+            const uint32_t c = (cw[k] & 0xffffu) + 1u;  // owners are candidate entries
+            const uint32_t x = cw[k] >> 16;
+            if (w[k] == static_cast<uint32_t>(i0 + k)) hits += c < x ? c : x;
+            if (i0 >= roff || x != 0) lm |= 1u << k;
+          }
+        }
+        // the quads of a warp can straddle the two parts: one append per part
+        const bool cside = qi < mcq;
+        warp_append_quad(lout, &s_nc, cside ? lm : 0u, [&](int k) { return pos[k]; }, lane);
+        warp_append_quad(lout + roff, &s_nr, cside ? 0u : lm, [&](int k) { return pos[k]; }, lane);
+      }
+      hits = __reduce_add_sync(kFull, hits);
+      if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+      cleared = true;
+      __syncthreads();
+      nc = s_nc;
+      nr = s_nr;
+      uint16_t* const t = lin;
+      lin = lout;
+      lout = t;
+      TB_MARK(3 + 4 * (n - 1) + 3);
+      ++n;
+    }
+    if (nc > 0 && n <= N) {
+      // Few survivors: warp 0 finishes the remaining orders with match.any on the
+      // keys.  An n-gram's id for the next order is the lowest lane holding it.
       if (tid < 32) {
-        int pos = lane < nsurv ? s_surv[lane] : -1;
+        int pos = lane < nc ? lin[lane] : (lane < nc + nr ? lin[roff + lane - nc] : -1);
         uint32_t pid = pos >= 0 ? idn[pos] : 0u;
-        for (int m = 2; m <= N; ++m) {
+        for (int m = n; m <= N; ++m) {
           bool valid = pos >= 0;
           uint32_t key = 0;
           if (valid) {
@@ -1809,106 +2098,6 @@ __global__ void __launch_bounds__(kThreads, 4)
           pid = static_cast<uint32_t>(leader);
         }
         __syncwarp();
-      }
-    } else if (nsurv > 32) {
-      // Many survivors: the same store-then-verify table per order, over position
-      // quads whose (n-1)-gram is still live (idn != 0xffff).
-      for (int n = 2; n <= N && nsurv; ++n) {
-        for (uint32_t s = tid; s < cap / 8; s += kThreads)
-          reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
-        for (int qi = tid; qi < nq; qi += kThreads) {  // keys of eligible positions
-          int p0;
-          const uint32_t vm = quad(qi, p0);
-          const int end = p0 < roff ? clen : roff + rlen;
-          uint32_t key[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int pos = p0 + k;
-            key[k] = ~0u;
-            if (vm >> k & 1u) {
-              const uint16_t pre = idn[pos];
-              const int q = pos + n - 1;
-              if (pre != 0xffffu && q < end) {
-                const uint16_t last = id1[q];
-                if (last != 0xffffu) key[k] = (static_cast<uint32_t>(pre) << 16) | last;
-              }
-            }
-          }
-          *reinterpret_cast<uint4*>(kc + p0) = make_uint4(key[0], key[1], key[2], key[3]);
-          *reinterpret_cast<uint4*>(cnt + p0) = make_uint4(0, 0, 0, 0);
-        }
-        if (tid == 0) {
-          s_nlost = 0;
-          s_nsurv = 0;
-        }
-        __syncthreads();
-        for (int qi = tid; qi < nq; qi += kThreads) {
-          int p0;
-          quad(qi, p0);
-          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + p0);
-          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (key[k] != ~0u) own[(key[k] * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(p0 + k);
-        }
-        __syncthreads();
-        for (int qi = tid; qi < nq; qi += kThreads) {
-          int p0;
-          quad(qi, p0);
-          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + p0);
-          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
-          uint32_t lm = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (key[k] == ~0u) continue;
-            const int pos = p0 + k;
-            const uint32_t hk = key[k] * 0x9E3779B1u;
-            const uint32_t home = hk >> hshift;
-            const uint16_t w = own[home];
-            if (w != pos) {
-              if (kc[w] == key[k]) {
-                atomicAdd(&cnt[w], inc_of(pos));
-              } else {
-                lm |= 1u << k;
-                pair_retry_store(own, hk, 1, hshift, static_cast<uint16_t>(pos));
-              }
-            }
-            idn[pos] = static_cast<uint16_t>(home);
-          }
-          for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
-        }
-        __syncthreads();
-        if (s_nlost)
-          pair_resolve_lost(own, cnt, lost, s_nlost, idn, mask, hshift, roff, tid,
-                            [&](uint16_t q) { return kc[q] * 0x9E3779B1u; },
-                            [&](uint16_t a, uint16_t b) { return kc[a] == kc[b]; });
-        unsigned int hits = 0;
-        bool live_c = false;
-        for (int qi = tid; qi < nq; qi += kThreads) {
-          int p0;
-          quad(qi, p0);
-          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + p0);
-          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int pos = p0 + k;
-            bool ok = false;
-            if (key[k] != ~0u) {
-              const uint32_t o = own[idn[pos]];
-              const uint32_t cw = cnt[o];
-              const uint32_t c = (cw & 0xffffu) + (o < static_cast<uint32_t>(roff) ? 1u : 0u);
-              const uint32_t x = (cw >> 16) + (o >= static_cast<uint32_t>(roff) ? 1u : 0u);
-              ok = pos < roff ? x != 0 : c != 0;
-              if (o == static_cast<uint32_t>(pos)) hits += c < x ? c : x;
-            }
-            if (!ok) idn[pos] = 0xffffu;
-            live_c |= ok && pos < roff;
-          }
-        }
-        hits = __reduce_add_sync(kFull, hits);
-        if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
-        nsurv = __syncthreads_count(live_c);
-        TB_MARK(3 + 4 * (n - 1) + 3);
       }
     }
 
@@ -2530,6 +2719,7 @@ struct Plan {
   bool pair = false;   // single-reference kernel
   bool multi = false;  // multi-reference kernel
   int cap_log2 = 0;
+  int filter_log2 = 0;
   int cand_pad = 0;
   int ref_off[TB_MAX_REFS + 1] = {0};
   int off_id1 = 0, off_idn = 0, off_live = 0, off_ent = 0, off_mref = 0, off_kc = 0, off_lists = 0, off_seg = 0;
@@ -2580,27 +2770,42 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       o = round_up(o + ptot * 2, 16);
       offs[2] = o;                       // own (u16 per slot)
       o = round_up(o + c * 2, 16);
-      offs[3] = o;                       // cnt (u32 per position)
+      offs[3] = o;                       // cnt (u32 per candidate position / entry)
+      o = round_up(o + cpad4 * 4, 16);
+      offs[4] = o;                       // two position lists (u16 per position each)
       o = round_up(o + ptot * 4, 16);
-      offs[4] = o;                       // lost-position list (u16 per position)
-      o = round_up(o + ptot * 2, 16);
       offs[5] = o;
       return o;
     };
-    // table load factor <= 1/4 when four CTAs still fit per SM, else <= 1/2
-    int lg = cap_log2_for(4 * ptot, 6);
+    // only candidate keys are inserted (every order).  Table load factor <= 1/8
+    // of the candidate width, else <= 1/4, at kPairCtasPerSm CTAs per SM, else
+    // the same at 3 CTAs per SM, else <= 1/2.
+    auto fits = [&](int64_t t, int ctas) {
+      return t + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin / ctas;
+    };
     int64_t offs[6];
-    int64_t total = pair_layout(lg, offs);
-    while (total + static_cast<int64_t>(kStaticSmemReserve) > smem_optin / kPairCtasPerSm &&
-           (int64_t(1) << (lg - 1)) >= 2 * ptot) {
-      --lg;
-      total = pair_layout(lg, offs);
-    }
+    int lg = -1;
+    for (int ctas = kPairCtasPerSm; ctas >= 3 && lg < 0; --ctas)
+      for (int l = cap_log2_for(8 * cpad4, 6); l >= 6 && (int64_t(1) << l) >= 4 * cpad4; --l)
+        if (fits(pair_layout(l, offs), ctas)) {
+          lg = l;
+          break;
+        }
+    if (lg < 0) lg = cap_log2_for(2 * cpad4, 6);
+    const int64_t total = pair_layout(lg, offs);
     if (lg <= 16 && ptot <= 16384 && total + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin) {
       pl->smem_mode = true;
       pl->pair = true;
       pl->cand_pad = static_cast<int>(cpad4);
       pl->cap_log2 = lg;
+      // the order-1 filter's two bitmaps span the table and the count array
+      // (adjacent; neither is in use while filtering)
+      {
+        const int64_t words = ((int64_t(1) << lg) * 2 + cpad4 * 4) / 8;  // per side
+        int fl = 0;
+        while ((int64_t(2) << fl) <= words) ++fl;
+        pl->filter_log2 = fl;
+      }
       pl->ref_off[0] = 0;
       pl->ref_off[1] = static_cast<int>(rpad);
       pl->off_id1 = static_cast<int>(offs[0]);
@@ -2613,8 +2818,9 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       // second token buffer while they work on the current one — when that
       // buffer still fits kPairCtasPerSm CTAs per SM
       const int64_t tok2 = round_up(ptot * (token_bytes > 4 ? token_bytes : 4), 16);
-      if (batch > static_cast<int64_t>(kPairCtasPerSm) * sms &&
-          total + tok2 + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin / kPairCtasPerSm) {
+      int ctas = static_cast<int>(smem_optin / (total + static_cast<int64_t>(kStaticSmemReserve)));
+      ctas = ctas < kPairCtasPerSm ? ctas : kPairCtasPerSm;
+      if (ctas >= 1 && batch > static_cast<int64_t>(ctas) * sms && fits(total + tok2, ctas)) {
         pl->off_tok2 = static_cast<int>(total);
         pl->smem_bytes = static_cast<size_t>(total + tok2);
       }
@@ -2902,6 +3108,7 @@ static int stats_impl(int32_t token_bytes, const void* cand_ids, int64_t cand_ld
   prm.ws_flag = reinterpret_cast<int*>(ws + pl.acc_bytes - 256 + 4);
   prm.err = err_flag;
   prm.cap_log2 = pl.cap_log2;
+  prm.filter_log2 = pl.filter_log2;
   prm.cand_pad = pl.cand_pad;
   for (int r = 0; r <= num_refs; ++r) prm.ref_off[r] = pl.ref_off[r];
   prm.off_id1 = pl.off_id1;

@@ -192,6 +192,26 @@ def test_max_refs_and_long_orders():
         tb.sentence_bleu(cand, rb)
 
 
+@pytest.mark.parametrize("order", [5, 9, 13])
+def test_single_ref_long_orders_all_live_list_regimes(order):
+    """Single reference, max_order > 4: the live-list table orders hand over to
+    the warp match path, whose 64-bit keys cover three orders at a time (so
+    orders 5+ chain a new id).  Mutation rates from 0 to 1 give every survivor
+    count from none through <= 32 (warp path from order 2) to all positions."""
+    rng = np.random.default_rng(40 + order)
+    b, l = 96, 384
+    cid = rng.integers(0, 3000, (b, l))
+    clen = rng.integers(l // 2, l + 1, b)
+    rid = cid.copy()
+    rate = np.linspace(0.0, 1.0, b)[:, None]
+    mut = rng.random((b, l)) < rate
+    rid[mut] = rng.integers(0, 3000, size=int(mut.sum()))
+    rlen = np.clip(clen + rng.integers(-8, 9, b), 0, l)
+    rlen[:4] = clen[:4]  # identical rows: every n-gram of every order matches
+    rid[:4] = cid[:4]
+    _check_against_oracle(cid, clen, [(rid, rlen)], tb.BleuConfig(max_order=order, smoothing="floor"))
+
+
 def test_huge_token_ids_and_negative_padding():
     rng = np.random.default_rng(12)
     b, l = 32, 300
