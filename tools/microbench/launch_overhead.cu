@@ -11,6 +11,11 @@
 #include "tensorbleu.h"
 
 __global__ void empty_kernel() {}
+// completion by a flag in mapped pinned memory (host spins instead of syncing)
+__global__ void flag_kernel(volatile unsigned* flag, unsigned seq) {
+  __threadfence_system();
+  *flag = seq;
+}
 
 template <typename F>
 double time_us(F f, int reps = 2000) {
@@ -82,6 +87,29 @@ int main() {
     printf("empty kernel event-timed       %7.2f us\n", tot * 1000 / 200);
   }
   printf("empty stream sync              %7.2f us\n", time_us([&] { cudaStreamSynchronize(st); }));
+  {
+    unsigned* hflag;
+    cudaHostAlloc(&hflag, 64, cudaHostAllocMapped);
+    unsigned* dflag;
+    cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflag), hflag, 0);
+    unsigned seq = 0;
+    *hflag = 0;
+    printf("flag kernel + host spin        %7.2f us\n", time_us([&] {
+      ++seq;
+      flag_kernel<<<1, 32, 0, st>>>(dflag, seq);
+      while (*reinterpret_cast<volatile unsigned*>(hflag) != seq) {
+      }
+    }));
+    cudaStreamSynchronize(st);
+    printf("flag kernel + sync             %7.2f us\n", time_us([&] {
+      ++seq;
+      flag_kernel<<<1, 32, 0, st>>>(dflag, seq);
+      cudaStreamSynchronize(st);
+    }));
+    unsigned* hflag2;
+    cudaHostAlloc(&hflag2, 64, cudaHostAllocMapped);
+    printf("host->pinned write + read      %7.2f us\n", time_us([&] { *reinterpret_cast<volatile unsigned*>(hflag2) = seq; }));
+  }
   int64_t *h_ids, *h_len;
   cudaHostAlloc(&h_ids, B * L * 8, 0);
   cudaHostAlloc(&h_len, B * 8, 0);
