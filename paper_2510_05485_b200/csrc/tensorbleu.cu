@@ -2170,9 +2170,8 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
   __shared__ int64_t s_stage_len[kMultiMaxRefs + 1];
   __shared__ unsigned long long s_tot[2 * TB_MAX_ORDER + 2];
   __shared__ int s_last, s_flags;
-  __shared__ int s_nlost, s_nsurv, s_ndef;
+  __shared__ int s_nlost, s_nc, s_nr, s_ndef;  // s_nc / s_nr: live candidate / reference entries
   __shared__ int s_qbase[kMultiMaxRefs + 2];  // first flattened reference quad of each reference (+ total)
-  __shared__ uint16_t s_surv[kSmallSet];   // live positions, when there are at most kSmallSet
   __shared__ uint32_t s_skey[kSmallSet];   // small-set path: their keys at the current order
   __shared__ uint8_t s_sside[kSmallSet];   // small-set path: 0 = candidate, 1 + r = reference r
   __shared__ int64_t s_effref;             // effective reference length of the current group
@@ -2195,8 +2194,14 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
   uint16_t* own = reinterpret_cast<uint16_t*>(smem + p.off_ent);   // slot -> owner (candidate) position
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + p.off_mref);  // candidate owner -> candidate count
   uint32_t* rc = reinterpret_cast<uint32_t*>(smem + p.off_kc);     // (ref, candidate owner) -> u16 count, 2 per word
-  uint16_t* lost = reinterpret_cast<uint16_t*>(smem + p.off_lists);  // lost candidates [0, cpad), deferred refs after
-  uint16_t* defl = lost + cpad;
+  // two position lists of ptot entries (as in the pair kernel): the live
+  // positions of an order (candidates from 0, references from cpad) and the
+  // lost (from 0) / deferred (from cpad) entries of the current order
+  const int ptot = cpad + p.ref_off[R];
+  uint16_t* const lx = reinterpret_cast<uint16_t*>(smem + p.off_lists);
+  uint16_t* const ly = lx + ptot;
+  uint16_t* const lost = ly;
+  uint16_t* const defl = ly + cpad;
   const uint32_t hshift = 32 - cap_log2;
   const uint32_t mask = cap - 1;
 
@@ -2256,16 +2261,16 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
       const int left = static_cast<int>(s_len[r + 1]) - j;
       return left >= 4 ? 0xfu : ((1u << left) - 1u);
     };
+    auto ref_of = [&](int pos) -> int {  // reference index of a reference position
+      int r = 0;  // independent compares against the row starts (no dependent chain)
+#pragma unroll
+      for (int j = 1; j < kMultiMaxRefs; ++j) r += (j < R && pos >= cpad + p.ref_off[j]) ? 1 : 0;
+      return r;
+    };
     auto row_end = [&](int pos) -> int {  // one past the last valid position of pos's row
       if (pos < cpad) return clen;
-      int r = 0;
-      while (r + 1 < R && pos >= cpad + p.ref_off[r + 1]) ++r;
+      const int r = ref_of(pos);
       return cpad + p.ref_off[r] + static_cast<int>(s_len[r + 1]);
-    };
-    auto ref_of = [&](int pos) -> int {  // reference index of a reference position
-      int r = 0;
-      while (r + 1 < R && pos >= cpad + p.ref_off[r + 1]) ++r;
-      return r;
     };
     auto rc_add = [&](int r, uint32_t o) {
       const uint32_t i = static_cast<uint32_t>(r * cpad) + o;
@@ -2283,9 +2288,8 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
     __syncthreads();  // s_qbase
     const int nrq = s_qbase[R];
 
-    // One order: keys of the valid / live positions (K = token type at order 1,
-    // packed u32 keys after), ids -> slot or 0xffff.  Returns (via s_nsurv /
-    // s_surv) the live positions.  All threads call it.
+    // Order 1 on the tokens (K = token type): ids -> slot or 0xffff; the live
+    // positions go to the list lx (s_nc / s_nr entries).  All threads call it.
     auto count_order = [&](auto* keys, uint16_t* ids, uint16_t* ids2, int n, bool order1) {
       using K = typename std::remove_const<typename std::remove_pointer<decltype(keys)>::type>::type;
       auto load_keys = [&](int p0, K (&k)[4]) {
@@ -2318,7 +2322,8 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
       if (tid == 0) {
         s_nlost = 0;
         s_ndef = 0;
-        s_nsurv = 0;
+        s_nc = 0;
+        s_nr = 0;
       }
       __syncthreads();
       for (int qi = tid; qi < ncq; qi += NT) {  // claims (plain stores)
@@ -2388,8 +2393,11 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
           pair_retry_store(own, h, 2, hshift, pos);
         }
       }
-      for (int qi = tid; qi < nrq; qi += NT) {  // ... with the home-slot lookups of all references
-        int r, p0;
+      for (int q0 = 0; q0 < nrq; q0 += NT) {  // ... with the home-slot lookups of all references
+        const int qi = q0 + tid;
+        int r = 0, p0 = 0;
+        uint32_t fm = 0;  // found: live
+        if (qi < nrq) {
         const uint32_t vm0 = ref_quad(qi, r, p0);
         K k[4];
         load_keys(p0, k);
@@ -2413,36 +2421,45 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
             v[j] = 0xffffu;
           } else {
             rc_add(r, o[j]);
-            const int s = atomicAdd(&s_nsurv, 1);
-            if (s < kSmallSet) s_surv[s] = static_cast<uint16_t>(p0 + j);
+            fm |= 1u << j;
           }
         }
         const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
         *reinterpret_cast<uint2*>(ids + p0) = vv;
         if (ids2) *reinterpret_cast<uint2*>(ids2 + p0) = vv;
+        }
+        warp_append_quad(lx + cpad, &s_nr, fm, [&](int j) { return p0 + j; }, lane);
       }
       if (__syncthreads_or(left))
         pair_resolve_lost<NT>(own, cnt, lost, nl, ids, mask, hshift, cpad, tid, hashk, eqk, 2);
       if (n == 1) TB_MARK(3);
       const int nd = s_ndef;
-      for (int i = tid; i < nd; i += NT) {  // deferred lookups: the full chain
-        const uint16_t pos = defl[i];
-        const K key = keys[pos];
-        uint16_t o;
-        const int sl = pair_find_retry(own, keys, key, tok_hash32(key), hshift, mask, &o);
-        if (sl >= 0) {
-          rc_add(ref_of(pos), o);
-          ids[pos] = static_cast<uint16_t>(sl);
-          if (ids2) ids2[pos] = static_cast<uint16_t>(sl);
-          const int s = atomicAdd(&s_nsurv, 1);
-          if (s < kSmallSet) s_surv[s] = pos;
+      for (int i0 = 0; i0 < nd; i0 += NT) {  // deferred lookups: the full chain
+        const int i = i0 + tid;
+        bool f = false;
+        int pos = 0;
+        if (i < nd) {
+          pos = defl[i];
+          const K key = keys[pos];
+          uint16_t o;
+          const int sl = pair_find_retry(own, keys, key, tok_hash32(key), hshift, mask, &o);
+          if (sl >= 0) {
+            rc_add(ref_of(pos), o);
+            ids[pos] = static_cast<uint16_t>(sl);
+            if (ids2) ids2[pos] = static_cast<uint16_t>(sl);
+            f = true;
+          }
         }
+        warp_append(lx + cpad, &s_nr, f, pos, lane);
       }
       __syncthreads();
       if (n == 1) TB_MARK(26);
       unsigned int hits = 0;
-      for (int qi = tid; qi < ncq; qi += NT) {  // candidate liveness + clipped count
+      for (int q0 = 0; q0 < ncq; q0 += NT) {  // candidate liveness + clipped count
+        const int qi = q0 + tid;
         const int p0 = 4 * qi;
+        uint32_t lm = 0;
+        if (qi < ncq) {
         K k[4];
         load_keys(p0, k);
         const uint32_t vm = live_mask(cand_mask(p0), k);
@@ -2462,14 +2479,15 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
             }
             if (x != 0) {
               v[j] = s[j];
-              const int q = atomicAdd(&s_nsurv, 1);
-              if (q < kSmallSet) s_surv[q] = static_cast<uint16_t>(pos);
+              lm |= 1u << j;
             }
           }
         }
         const uint2 vv = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
         *reinterpret_cast<uint2*>(ids + p0) = vv;
         if (ids2) *reinterpret_cast<uint2*>(ids2 + p0) = vv;
+        }
+        warp_append_quad(lx, &s_nc, lm, [&](int j) { return p0 + j; }, lane);
       }
       hits = __reduce_add_sync(kFull, hits);
       if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
@@ -2479,47 +2497,206 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
     // ================= order 1: tokens =================
     count_order(static_cast<const T*>(tok), id1, idn, 1, true);
     TB_MARK(4);
-    int nsurv = s_nsurv;
+    int nc = s_nc, nr = s_nr;
 
     // ================= orders n >= 2 =================
+    // While more than kSmallSet positions stay live: one table round per order
+    // over the live LISTS, in quads of entries (the pair kernel's rounds, with
+    // the per-reference counts rc[r][owner] and the clip min(cand, max_r ref)).
+    // Owners, counts and the next prefix ids are list indices.
+    uint16_t* lin = lx;
+    uint16_t* lout = ly;
     int n = 2;
-    for (; n <= N && nsurv > kSmallSet; ++n) {
-      // packed keys of the positions whose (n-1)-prefix and last token are live
-      const int nq_all = ncq + nrq;
-      for (int qi = tid; qi < nq_all; qi += NT) {
-        int r = 0, p0 = 4 * qi;
-        const uint32_t vm = qi < ncq ? cand_mask(p0) : ref_quad(qi - ncq, r, p0);
-        const int end = row_end(p0);
+    bool cleared = false;  // own[] still holds order 1's table
+    while (__builtin_expect(n <= N && nc > 0 && nc + nr > kSmallSet, 0)) {
+      const int mcq = (nc + 3) >> 2;
+      const int mq = mcq + ((nr + 3) >> 2);
+      auto equad = [&](int qi, int& i0) -> uint32_t {
+        int left;
+        if (qi < mcq) {
+          i0 = 4 * qi;
+          left = nc - i0;
+        } else {
+          i0 = cpad + 4 * (qi - mcq);
+          left = nr - (i0 - cpad);
+        }
+        return left >= 4 ? 0xfu : ((1u << left) - 1u);
+      };
+      auto lpos = [&](int i0, int (&pos)[4]) {
+        const uint2 l2 = *reinterpret_cast<const uint2*>(lin + i0);
+        pos[0] = l2.x & 0xffffu;
+        pos[1] = l2.x >> 16;
+        pos[2] = l2.y & 0xffffu;
+        pos[3] = l2.y >> 16;
+      };
+      if (!cleared)
+        for (uint32_t s = tid; s < cap / 8; s += NT) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      for (int qi = tid; qi < mq; qi += NT) {  // keys (~0: dead), counts, candidate claims
+        int i0;
+        const uint32_t vm = equad(qi, i0);
+        int pos[4];
+        lpos(i0, pos);
         uint32_t key[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int pos = p0 + j;
           key[j] = ~0u;
           if (vm >> j & 1u) {
-            const uint16_t pre = idn[pos];
-            const int q = pos + n - 1;
-            if (pre != 0xffffu && q < end) {
-              const uint16_t last = id1[q];
-              if (last != 0xffffu) key[j] = (static_cast<uint32_t>(pre) << 16) | last;
+            const int q = pos[j] + n - 1;
+            if (q < row_end(pos[j])) {
+              const uint16_t l = id1[q];
+              if (l != 0xffffu) key[j] = (static_cast<uint32_t>(idn[pos[j]]) << 16) | l;
             }
           }
         }
-        *reinterpret_cast<uint4*>(kc + p0) = make_uint4(key[0], key[1], key[2], key[3]);
+        *reinterpret_cast<uint4*>(kc + i0) = make_uint4(key[0], key[1], key[2], key[3]);
+        if (i0 < cpad) {
+          *reinterpret_cast<uint4*>(cnt + i0) = make_uint4(0, 0, 0, 0);
+          for (int r = 0; r < R; ++r)  // rc[r][i0 .. i0 + 3]: 4 u16, 8-byte aligned (cpad % 4 == 0)
+            *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(rc) + r * cpad + i0) = make_uint2(0, 0);
+          if (cleared) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (key[j] != ~0u) own[(key[j] * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(i0 + j);
+          }
+        }
+      }
+      if (tid == 0) {
+        s_nlost = 0;
+        s_ndef = 0;
       }
       __syncthreads();
-      count_order(static_cast<const uint32_t*>(kc), idn, static_cast<uint16_t*>(nullptr), n, false);
-      nsurv = s_nsurv;
+      if (!cleared) {
+        for (int qi = tid; qi < mcq; qi += NT) {
+          const int i0 = 4 * qi;
+          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + i0);
+          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (key[j] != ~0u) own[(key[j] * 0x9E3779B1u) >> hshift] = static_cast<uint16_t>(i0 + j);
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {  // every thread has read them (barrier above)
+        s_nc = 0;
+        s_nr = 0;
+      }
+      uint16_t* const ldef = lout + cpad;  // deferred reference entries (lost candidates from 0)
+      for (int qi = tid; qi < mq; qi += NT) {  // verify (candidates) / home lookups (references)
+        int i0;
+        equad(qi, i0);
+        int pos[4];
+        lpos(i0, pos);
+        const uint4 k4 = *reinterpret_cast<const uint4*>(kc + i0);
+        const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+        uint16_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = key[j] != ~0u ? own[(key[j] * 0x9E3779B1u) >> hshift] : 0xffffu;
+        uint32_t kw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) kw[j] = w[j] != 0xffffu ? kc[w[j]] : ~0u;
+        if (i0 < cpad) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (key[j] == ~0u) continue;
+            const int i = i0 + j;
+            if (w[j] == i) {
+              idn[pos[j]] = static_cast<uint16_t>(i);
+            } else if (kw[j] == key[j]) {
+              atomicAdd(&cnt[w[j]], 1u);
+              idn[pos[j]] = w[j];
+            } else {
+              lout[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(i);
+              pair_retry_store(own, key[j] * 0x9E3779B1u, 1, hshift, static_cast<uint16_t>(i));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (key[j] == ~0u) continue;
+            const int i = i0 + j;
+            if (w[j] == 0xffffu) {  // empty home: no candidate n-gram has this key
+              kc[i] = ~0u;
+            } else if (kw[j] == key[j]) {
+              rc_add(ref_of(pos[j]), w[j]);
+              idn[pos[j]] = w[j];
+            } else {
+              ldef[atomicAdd(&s_ndef, 1)] = static_cast<uint16_t>(i);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (s_nlost) list_resolve_lost<NT>(own, cnt, kc, lout, s_nlost, lin, idn, mask, hshift, tid);
+      if (s_ndef) {
+        const int nd = s_ndef;
+        for (int j = tid; j < nd; j += NT) {
+          const uint16_t i = ldef[j];
+          const uint32_t key = kc[i];
+          uint16_t w;
+          if (pair_find_retry(own, kc, key, key * 0x9E3779B1u, hshift, mask, &w) >= 0) {
+            rc_add(ref_of(lin[i]), w);
+            idn[lin[i]] = w;
+          } else {
+            kc[i] = ~0u;
+          }
+        }
+        __syncthreads();
+      }
+      // live: clipped counts (owners), survivors to lout, the table cleared
+      if (n < N)
+        for (uint32_t s = tid; s < cap / 8; s += NT) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      unsigned int hits = 0;
+      for (int q0 = 0; q0 < mq; q0 += NT) {
+        const int qi = q0 + tid;
+        int i0 = 0;
+        uint32_t lm = 0;
+        int pos[4] = {0, 0, 0, 0};
+        if (qi < mq) {
+          equad(qi, i0);
+          lpos(i0, pos);
+          const uint4 k4 = *reinterpret_cast<const uint4*>(kc + i0);
+          const uint32_t key[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (key[j] == ~0u) continue;
+            if (i0 >= cpad) {
+              lm |= 1u << j;
+              continue;
+            }
+            const uint32_t w = idn[pos[j]];
+            const uint32_t x = rc_max(w);
+            if (w == static_cast<uint32_t>(i0 + j)) {
+              const uint32_t c = (cnt[w] & 0xffffu) + 1u;  // owners are candidate entries
+              hits += c < x ? c : x;
+            }
+            if (x != 0) lm |= 1u << j;
+          }
+        }
+        const bool cside = qi < mcq;
+        warp_append_quad(lout, &s_nc, cside ? lm : 0u, [&](int j) { return pos[j]; }, lane);
+        warp_append_quad(lout + cpad, &s_nr, cside ? 0u : lm, [&](int j) { return pos[j]; }, lane);
+      }
+      hits = __reduce_add_sync(kFull, hits);
+      if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+      cleared = true;
+      __syncthreads();
+      nc = s_nc;
+      nr = s_nr;
+      uint16_t* const t = lin;
+      lin = lout;
+      lout = t;
+      ++n;
     }
-    if (n <= N && nsurv > 0) {
+    if (n <= N && nc > 0) {
       // <= kSmallSet live positions: the remaining orders by direct comparison
       // of their keys (S^2 / blockDim compares per thread, two barriers per
       // order, no table).  An n-gram's id for the next order is the lowest
       // index holding it.
-      const int S = nsurv;
+      const int S = nc + nr;
       int pos = -1, side = 0, end = 0;
       uint32_t pid = 0;
       if (tid < S) {
-        pos = s_surv[tid];
+        pos = tid < nc ? lin[tid] : lin[cpad + tid - nc];
         side = pos < cpad ? 0 : 1 + ref_of(pos);
         end = row_end(pos);
         pid = idn[pos];
@@ -2853,8 +3030,8 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       q = round_up(q + cpad4 * 4, 16);
       offs[4] = q;                          // rc (u16 per reference x candidate position)
       q = round_up(q + R * cpad4 * 2, 16);
-      offs[5] = q;                          // lost candidates + deferred reference positions (u16)
-      q = round_up(q + ptot * 2, 16);
+      offs[5] = q;                          // two position lists (u16 per position each)
+      q = round_up(q + ptot * 4, 16);
       return q;
     };
     // table load <= 1/8 of the candidate positions while two CTAs fit per SM

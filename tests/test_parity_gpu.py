@@ -209,7 +209,30 @@ def test_single_ref_long_orders_all_live_list_regimes(order):
     rlen = np.clip(clen + rng.integers(-8, 9, b), 0, l)
     rlen[:4] = clen[:4]  # identical rows: every n-gram of every order matches
     rid[:4] = cid[:4]
-    _check_against_oracle(cid, clen, [(rid, rlen)], tb.BleuConfig(max_order=order, smoothing="floor"))
+    for dt in (torch.int32, torch.int64):
+        _check_against_oracle(cid, clen, [(rid, rlen)], tb.BleuConfig(max_order=order, smoothing="floor"), dtype=dt)
+
+
+@pytest.mark.parametrize("R,order", [(2, 4), (3, 7), (8, 5)])
+def test_multi_ref_live_list_rounds(R, order):
+    """2 <= R <= 8: the live-list table rounds of orders >= 2 (more than 128
+    live positions), the hand-over to the small-set path, and every survivor
+    regime from identical rows (all live at every order) to unrelated rows."""
+    rng = np.random.default_rng(70 + R + order)
+    b, l = 64, 320
+    cid = rng.integers(0, 4000, (b, l))
+    clen = rng.integers(l // 2, l + 1, b)
+    refs = []
+    for r in range(R):
+        rid = cid.copy()
+        mut = rng.random((b, l)) < np.linspace(0.0, 1.0, b)[:, None] * (0.5 + 0.5 * r / R)
+        rid[mut] = rng.integers(0, 4000, size=int(mut.sum()))
+        rlen = np.clip(clen + rng.integers(-6, 7, b), 0, l)
+        if r == 0:
+            rid[:3], rlen[:3] = cid[:3], clen[:3]
+        refs.append((rid, rlen))
+    for dt in (torch.int32, torch.int64):
+        _check_against_oracle(cid, clen, refs, tb.BleuConfig(max_order=order, smoothing="add-k"), dtype=dt)
 
 
 def test_huge_token_ids_and_negative_padding():
