@@ -468,6 +468,7 @@ __device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int&
     return;
   }
   const int nt = 2 * N + 2;
+  __syncthreads();  // s_tot of the last group (warp 0's epilogue) before other threads read it
   if (corpus && tid < nt && s_tot[tid]) atomicAdd(&p.acc[(blockIdx.x % kAccCopies) * nt + tid], s_tot[tid]);
   if (tid == 0 && s_flags) atomicOr(p.ws_flag, s_flags);
   __syncthreads();

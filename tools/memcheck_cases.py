@@ -40,11 +40,15 @@ def main():
         dict(b=2, l=20000, v=40, r=1),                   # global-memory kernel
         dict(b=30, l=100, v=1000, r=1, pinned=True),     # host prefix mode
         dict(b=30, l=100, v=1000, r=2, pinned=True),
+        dict(b=700, l=48, v=100000, r=1),                # pair, several groups per CTA (prefetch buffer)
+        dict(b=700, l=48, v=30, r=1, corr=True),         # the same on the hash passes / list rounds
     ]
     for c in cases:
         cand, refs = batch(rng, **c)
         tb.sentence_bleu(cand, refs, tb.BleuConfig(smoothing="exp"))
         tb.corpus_bleu(cand, refs)
+        if c.get("corr"):  # long orders: list rounds beyond order 4, warp-path hand-over
+            tb.sentence_bleu(cand, refs, tb.BleuConfig(max_order=9, smoothing="floor"))
     d = torch.device("cuda", 0)
     cand, refs = batch(rng, 64, 128, 500, 1, dev=d)
     tb.compute_stats(cand, refs, tb.BleuConfig())
