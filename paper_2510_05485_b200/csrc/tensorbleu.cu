@@ -2291,7 +2291,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
 
     // Order 1 on the tokens (K = token type): ids -> slot or 0xffff; the live
     // positions go to the list lx (s_nc / s_nr entries).  All threads call it.
-    auto count_order = [&](auto* keys, uint16_t* ids, uint16_t* ids2, int n, bool order1) {
+    auto count_order1 = [&](auto* keys, uint16_t* ids, uint16_t* ids2) {
       using K = typename std::remove_const<typename std::remove_pointer<decltype(keys)>::type>::type;
       auto load_keys = [&](int p0, K (&k)[4]) {
         if constexpr (sizeof(K) == 4) {
@@ -2309,14 +2309,6 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
           k[3] = v.y;
         }
       };
-      auto live_mask = [&](uint32_t vm, const K (&k)[4]) -> uint32_t {
-        if (order1) return vm;
-        uint32_t m = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if ((vm >> j & 1u) && static_cast<uint32_t>(k[j]) != ~0u) m |= 1u << j;
-        return m;
-      };
       // table, candidate counts and per-reference counts start empty
       for (uint32_t s = tid; s < cap / 8; s += NT) reinterpret_cast<uint4*>(own)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
       for (int i = tid; i < (R * cpad + 7) / 8; i += NT) reinterpret_cast<uint4*>(rc)[i] = make_uint4(0, 0, 0, 0);
@@ -2331,19 +2323,19 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         const int p0 = 4 * qi;
         K k[4];
         load_keys(p0, k);
-        const uint32_t vm = live_mask(cand_mask(p0), k);
+        const uint32_t vm = cand_mask(p0);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (vm >> j & 1u) own[tok_hash32(k[j]) >> hshift] = static_cast<uint16_t>(p0 + j);
         *reinterpret_cast<uint4*>(cnt + p0) = make_uint4(0, 0, 0, 0);
       }
       __syncthreads();
-      if (n == 1) TB_MARK(28);
+      TB_MARK(28);
       for (int qi = tid; qi < ncq; qi += NT) {  // verify
         const int p0 = 4 * qi;
         K k[4];
         load_keys(p0, k);
-        const uint32_t vm = live_mask(cand_mask(p0), k);
+        const uint32_t vm = cand_mask(p0);
         uint32_t hv[4], home[4];
         uint16_t w[4];
 #pragma unroll
@@ -2369,13 +2361,13 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         *reinterpret_cast<uint2*>(ids + p0) = make_uint2(home[0] | (home[1] << 16), home[2] | (home[3] << 16));
         for (; lm; lm &= lm - 1) lost[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(p0 + __ffs(lm) - 1);
       }
-      if (order1 && tid == NT - 32) {  // lengths only: the last warp, off the epilogue's critical path
+      if (tid == NT - 32) {  // lengths only: the last warp, off the epilogue's critical path
         const int64_t r = closest_ref_len(s_len[0], &s_len[1], R);
         s_effref = r;
         s_bp = brevity_penalty_fp64(s_len[0], r);
       }
       __syncthreads();
-      if (n == 1) TB_MARK(29);
+      TB_MARK(29);
       const int nl = s_nlost;
       auto hashk = [&](uint16_t q) { return tok_hash32(keys[q]); };
       auto eqk = [&](uint16_t a, uint16_t c) { return keys[a] == keys[c]; };
@@ -2402,7 +2394,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         const uint32_t vm0 = ref_quad(qi, r, p0);
         K k[4];
         load_keys(p0, k);
-        const uint32_t vm = live_mask(vm0, k);
+        const uint32_t vm = vm0;
         uint32_t v[4];
         uint16_t o[4];
 #pragma unroll
@@ -2433,7 +2425,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
       }
       if (__syncthreads_or(left))
         pair_resolve_lost<NT>(own, cnt, lost, nl, ids, mask, hshift, cpad, tid, hashk, eqk, 2);
-      if (n == 1) TB_MARK(3);
+      TB_MARK(3);
       const int nd = s_ndef;
       for (int i0 = 0; i0 < nd; i0 += NT) {  // deferred lookups: the full chain
         const int i = i0 + tid;
@@ -2454,7 +2446,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         warp_append(lx + cpad, &s_nr, f, pos, lane);
       }
       __syncthreads();
-      if (n == 1) TB_MARK(26);
+      TB_MARK(26);
       unsigned int hits = 0;
       for (int q0 = 0; q0 < ncq; q0 += NT) {  // candidate liveness + clipped count
         const int qi = q0 + tid;
@@ -2463,7 +2455,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         if (qi < ncq) {
         K k[4];
         load_keys(p0, k);
-        const uint32_t vm = live_mask(cand_mask(p0), k);
+        const uint32_t vm = cand_mask(p0);
         const uint2 s2 = *reinterpret_cast<const uint2*>(ids + p0);
         const uint32_t s[4] = {s2.x & 0xffffu, s2.x >> 16, s2.y & 0xffffu, s2.y >> 16};
         uint32_t v[4];
@@ -2491,12 +2483,12 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         warp_append_quad(lx, &s_nc, lm, [&](int j) { return p0 + j; }, lane);
       }
       hits = __reduce_add_sync(kFull, hits);
-      if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
+      if (lane == 0 && hits) atomicAdd(&s_hits[0], hits);
       __syncthreads();
     };
 
     // ================= order 1: tokens =================
-    count_order(static_cast<const T*>(tok), id1, idn, 1, true);
+    count_order1(static_cast<const T*>(tok), id1, idn);
     TB_MARK(4);
     int nc = s_nc, nr = s_nr;
 
