@@ -423,7 +423,10 @@ __device__ void warp_epilogue(int64_t num, int64_t den, int64_t c, int64_t r, in
   // takes the slow path of the fp64 divide (hundreds of cycles) even though its
   // result is discarded
   const double ds = has_den ? dd : 1.0;
-  double pn = has_den ? __ddiv_rn(nd, ds) : 0.0;
+  // 0 / den is +0 exactly; a zero numerator would also take the divide's slow
+  // path (its operand-range check fails for |x| < 2^-120), and one such lane
+  // stalls the warp for hundreds of cycles
+  double pn = (has_den && num != 0) ? __ddiv_rn(nd, ds) : 0.0;
   if (smoothing == TB_SMOOTH_FLOOR) {
     if (zero_num) pn = __ddiv_rn(eps, ds);
   } else if (smoothing == TB_SMOOTH_ADD_K) {

@@ -26,6 +26,8 @@ for n in range(2, 7):
     for k, nm in enumerate(["P0clear", "P1cand", "P2ref", "P3live"]):
         NAMES.setdefault(3 + 4 * (n - 1) + k, f"o{n}.{nm}")
 NAMES[24] = "orders>=2"
+NAMES[1] = "epi.stores"
+NAMES[23] = "epi.math"
 NAMES.update({20: "f.bitmaps", 21: "f.filter", 22: "f.match"})
 
 
