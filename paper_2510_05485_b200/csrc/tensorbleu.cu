@@ -25,8 +25,9 @@
 //     reference tokens look up; min(cand, ref) is added once per key by its
 //     owner;
 //   * orders >= 2 visit only n-grams whose (n-1)-prefix and last token matched:
-//     key = (slot of the prefix, slot of the last token); <= 32 live positions
-//     finish in one warp with match.any, more use the same table per order;
+//     key = (id of the prefix, order-1 id of the last token); <= 32 live
+//     positions finish in one warp with match.any, more run one table round
+//     per order over the LIST of live positions (three barrier phases);
 //   * bleu_multi_kernel (2 <= R <= 8): the same passes with one count per
 //     (reference, candidate owner), clip = min(cand, max_r ref_r);
 //     bleu_group_kernel (R > 8) walks the references one by one;
@@ -1203,19 +1204,24 @@ __global__ void __launch_bounds__(kThreads, 4)
 // --------------------------------------------------------------------------
 // Single-reference kernel (R == 1, the headline configuration).
 //
-// Candidate AND reference n-grams are inserted into one table, so there is no
-// separate lookup phase.  Insertion is store-then-verify:
-//   round 1: every position stores itself (u16) into its key's home slot —
-//            plain stores, one wins;
-//   round 2: the winner owns the slot (its own occurrence is counted
-//            implicitly); an equal key adds one to its side's count (the only
-//            atomic of the common path); a different key probes 8-slot
-//            buckets (one 16-byte load each) and CAS-inserts.
-// Per slot: owner position (u16) and one u32 word [ref count 16 | cand count 16]
-// excluding the owner.  The liveness pass adds min(cand, ref) once per slot
-// (by its owner) and keeps the positions whose n-gram occurs on the other
-// side; only those are extended at the next order (exact, see above).
-// Order-n keys live in `kc`, which aliases the token buffer (dead after order 1).
+// Order 1: a blocked two-bit Bloom filter per side (in the table + count
+// region) drops the tokens absent from the other side; when <= kSmallSet
+// positions survive (unrelated text) they are matched exactly without a
+// table.  Otherwise only CANDIDATE tokens are inserted, store-then-verify:
+//   claim:  every candidate position stores itself (u16) into its token's
+//           home slot — plain stores, one wins;
+//   verify: the winner owns the slot (its own occurrence is counted
+//           implicitly); an equal token adds one to the owner's count word
+//           [ref 16 | cand 16] (the only atomic of the common path); a
+//           different token is lost and retries in rounds with fresh hashes
+//           (plain stores again), then serial CAS probing for leftovers.
+// Reference tokens only look up (an absent token can neither be counted nor
+// start a matching n-gram).  The liveness pass adds min(cand, ref) once per
+// slot (by its owner) and lists the positions whose token occurs on the other
+// side; only those are extended at the next order (exact pruning).
+// Orders >= 2 run the same claim / verify-or-look-up / live rounds over that
+// list (owners, counts and next-order ids are list indices); their keys live
+// in `kc`, which aliases the token buffer (dead after order 1).
 // --------------------------------------------------------------------------
 // 32-bit CAS on a shared-memory address (explicit state space: the address is
 // computed with integer arithmetic, which would otherwise become a generic,
