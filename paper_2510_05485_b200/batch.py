@@ -139,7 +139,21 @@ class TokenBatch:
 
     @property
     def batch_size(self) -> int:
-        return int(self.ids.shape[0])
+        v = self.__dict__.get("_bs")  # cached: the batch is immutable (per-call overhead)
+        if v is None:
+            v = int(self.ids.shape[0])
+            object.__setattr__(self, "_bs", v)
+        return v
+
+    @property
+    def _tok32(self) -> bool:
+        """Token IDs are int32 (numpy or torch), cached."""
+        v = self.__dict__.get("_t32")
+        if v is None:
+            dt = self.ids.dtype
+            v = (dt is torch.int32) if isinstance(dt, torch.dtype) else (dt == np.int32)
+            object.__setattr__(self, "_t32", v)
+        return v
 
     @property
     def max_len(self) -> int:
@@ -147,7 +161,11 @@ class TokenBatch:
 
     @property
     def is_device(self) -> bool:
-        return _is_torch(self.ids) and self.ids.is_cuda
+        v = self.__dict__.get("_dev")
+        if v is None:
+            v = _is_torch(self.ids) and self.ids.is_cuda
+            object.__setattr__(self, "_dev", v)
+        return v
 
     @classmethod
     def from_lists(cls, sentences: Sequence[Sequence[int]], pad_value: int = 0,

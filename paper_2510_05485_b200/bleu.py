@@ -151,7 +151,6 @@ def _to_device(batch: TokenBatch, device: torch.device, want64: bool):
     return ids, lengths, ld
 
 
-_INT32 = (np.dtype(np.int32), torch.int32)
 _MODES = {"stats": 0, "sentence": 1, "corpus": 2}
 _OUT_NAMES = {"stats": ("num", "den", "cand_len", "eff_ref"),
               "sentence": ("scores", "precisions", "bp"),
@@ -165,9 +164,9 @@ def _launch_host(candidates: TokenBatch, references: Sequence[TokenBatch], confi
     kernel over PCIe (valid prefixes only); results come back as numpy."""
     hp = _native._hp or _native.hostpath()
     dev = _native.current_device_index()
-    want64 = candidates.ids.dtype not in _INT32
+    want64 = not candidates._tok32
     for b in references:
-        want64 = want64 or b.ids.dtype not in _INT32
+        want64 = want64 or not b._tok32
     views = (candidates._row_view(want64)[0], *[b._row_view(want64)[0] for b in references])
     smc, eps, k, waddr = _config_abi(config)
     rc, flags, *outs = hp.run(_MODES[mode], views, candidates.batch_size, config.max_order,
