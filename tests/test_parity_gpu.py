@@ -235,6 +235,23 @@ def test_multi_ref_live_list_rounds(R, order):
         _check_against_oracle(cid, clen, refs, tb.BleuConfig(max_order=order, smoothing="add-k"), dtype=dt)
 
 
+@pytest.mark.parametrize("l,v", [(3000, 200000), (6000, 500), (8190, 40)])
+def test_single_ref_wide_rows_big_shared_tables(l, v):
+    """R = 1 rows of 3k-8k tokens: the pair kernel at 1-3 CTAs per SM with
+    the largest tables and live lists (u16 positions up to ~16k), related and
+    unrelated rows, and rows too wide for it (the generic kernel)."""
+    rng = np.random.default_rng(l + v)
+    b = 6
+    cid = rng.integers(0, v, (b, l))
+    clen = np.array([l, l - 1, l // 2, 1, 0, l - 3])
+    rid = cid.copy()
+    mut = rng.random((b, l)) < np.array([0.0, 0.05, 0.5, 1.0, 0.3, 0.9])[:, None]
+    rid[mut] = rng.integers(0, v, size=int(mut.sum()))
+    rlen = np.array([l, l, l // 3, 5, 7, l - 100])
+    for dt in (torch.int32, torch.int64):
+        _check_against_oracle(cid, clen, [(rid, rlen)], tb.BleuConfig(smoothing="exp"), dtype=dt)
+
+
 def test_huge_token_ids_and_negative_padding():
     rng = np.random.default_rng(12)
     b, l = 32, 300
