@@ -6,7 +6,9 @@ Draws random shapes (batch, row widths per reference set, 1..12 references),
 vocabularies (1 .. 2^40), token dtypes, max orders (1..9), mutation rates
 (related and unrelated text) and lengths (including 0 and the full width),
 runs compute_stats on CUDA tensors and on pinned host tensors, and asserts the
-counts are bit-identical to the oracle.  Prints the first failing case with
+counts are bit-identical to the oracle and the fp64 scores (smoothing cycling
+through none / floor / add-k / exp) agree within 1e-12 relative with the
+same zero set.  Prints the first failing case with
 its seed and exits 1; otherwise the number of cases checked.  Not collected
 by pytest (test infrastructure driven by hand / tools/gpu_round.sh).
 """
@@ -50,16 +52,19 @@ def case(rng):
     return cid, clen, refs, n, dt
 
 
-def run(cid, clen, refs, n, dt, where):
+def run(cid, clen, refs, n, dt, where, smoothing="none"):
     if where == "cuda":
         mk = lambda i, ln: tb.TokenBatch(ids=torch.as_tensor(i).to(dt).cuda(),  # noqa: E731
                                          lengths=torch.as_tensor(ln).cuda())
     else:
         mk = lambda i, ln: tb.TokenBatch(ids=torch.as_tensor(i).to(dt).pin_memory(),  # noqa: E731
                                          lengths=torch.as_tensor(ln))
-    st = tb.compute_stats(mk(cid, clen), [mk(i, ln) for i, ln in refs], tb.BleuConfig(max_order=n))
+    cfg = tb.BleuConfig(max_order=n, smoothing=smoothing)
+    cand, rb = mk(cid, clen), [mk(i, ln) for i, ln in refs]
+    st = tb.compute_stats(cand, rb, cfg)
+    res = tb.sentence_bleu(cand, rb, cfg)
     f = lambda x: x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)  # noqa: E731
-    return f(st.numerators), f(st.denominators), f(st.eff_ref_lens)
+    return f(st.numerators), f(st.denominators), f(st.eff_ref_lens), f(res.scores)
 
 
 def main():
@@ -74,14 +79,19 @@ def main():
         rng = np.random.default_rng(seed)
         cid, clen, refs, n, dt = case(rng)
         o = oracle.stats(cid, clen, refs, n)
+        sm = ("none", "floor", "add-k", "exp")[k % 4]
+        os_ = oracle.scores(o, sm)["scores"]
         for where in ("cuda", "host"):
-            num, den, eff = run(cid, clen, refs, n, dt, where)
+            num, den, eff, sc = run(cid, clen, refs, n, dt, where, sm)
             ok = (np.array_equal(num, o["numerators"]) and np.array_equal(den, o["denominators"])
-                  and np.array_equal(eff, o["eff_ref_lens"]))
+                  and np.array_equal(eff, o["eff_ref_lens"])
+                  and np.array_equal(sc == 0, os_ == 0)
+                  and np.allclose(sc, os_, rtol=1e-12, atol=0))
             if not ok:
                 bad = np.nonzero((num != o["numerators"]).any(axis=1))[0]
                 print(f"MISMATCH seed={seed} where={where} B={cid.shape[0]} L={cid.shape[1]} R={len(refs)} "
-                      f"N={n} dtype={dt} rows={bad[:10].tolist()}")
+                      f"N={n} dtype={dt} smoothing={sm} rows={bad[:10].tolist()} "
+                      f"max score rel err {np.max(np.abs(sc - os_) / np.maximum(np.abs(os_), 1e-300)):.3g}")
                 sys.exit(1)
         k += 1
     print(f"fuzz ok: {k} cases x 2 paths in {time.time() - t0:.0f} s")
