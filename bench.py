@@ -422,11 +422,15 @@ def run_ours(args):
     # TokenBatch's own dtype, batch.py:23-24) is reported beside it.
     d2h = 4 + (b * (2 + cfg.max_order) * 8 if not corpus else (3 * cfg.max_order + 4) * 8)
 
-    def measure_e2e(np_dtype):
-        hcand = tb.TokenBatch(ids=torch.from_numpy(cand_np[0].astype(np_dtype)).pin_memory(),
-                              lengths=torch.from_numpy(cand_np[1]))
-        hrefs = [tb.TokenBatch(ids=torch.from_numpy(i.astype(np_dtype)).pin_memory(), lengths=torch.from_numpy(ln))
-                 for i, ln in refs_np]
+    def measure_e2e(np_dtype, numpy_rows=False):
+        if numpy_rows:  # the reference's usage: TokenBatch over (pageable) numpy arrays
+            hcand = tb.TokenBatch(ids=cand_np[0].astype(np_dtype), lengths=cand_np[1])
+            hrefs = [tb.TokenBatch(ids=i.astype(np_dtype), lengths=ln) for i, ln in refs_np]
+        else:
+            hcand = tb.TokenBatch(ids=torch.from_numpy(cand_np[0].astype(np_dtype)).pin_memory(),
+                                  lengths=torch.from_numpy(cand_np[1]))
+            hrefs = [tb.TokenBatch(ids=torch.from_numpy(i.astype(np_dtype)).pin_memory(), lengths=torch.from_numpy(ln))
+                     for i, ln in refs_np]
         # tb_bleu_host: the kernel reads each pinned row's valid prefix over PCIe
         # (zero-copy) plus the lengths; results are written straight into pinned memory
         isz = np.dtype(np_dtype).itemsize
@@ -460,6 +464,7 @@ def run_ours(args):
 
     e2e_value, h2d = measure_e2e(np.int32)
     e2e64_value, h2d64 = measure_e2e(np.int64)
+    e2e_np_value, _ = measure_e2e(np.int64, numpy_rows=True)
 
     # ---- roofline of the fused kernel (the only kernel of a step)
     a_bytes = algorithmic_bytes([cand_np[1]] + [ln for _, ln in refs_np], v, b)
@@ -520,6 +525,10 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "sentences/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "token_dtype": "int32",
                     "int64_tokens": {"value": e2e64_value, "h2d_bytes_per_step": int(h2d64)},
+                    "numpy_int64_tokens": {"value": e2e_np_value,
+                                           "path": "TokenBatch(numpy int64, pageable) as the reference uses it: "
+                                                   "valid prefixes copied into pinned memory by host threads, "
+                                                   "narrowed to int32 when the IDs fit, read over PCIe"},
                     "path": f"{'corpus' if corpus else 'sentence'}_bleu(TokenBatch(pinned host tensors)) "
                             "-> numpy: one blocking tb_bleu_host call; the kernel streams valid row prefixes "
                             "over PCIe" + (" (+ NCCL all_reduce of the totals)" if corpus and distributed else "")},

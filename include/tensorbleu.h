@@ -136,8 +136,12 @@ int tb_bleu_stats(int32_t token_bytes,
  *    cudaHostAlloc / torch pin_memory) or pageable, or device memory.  Pinned
  *    token rows are read by the kernel directly over PCIe — only the valid
  *    prefix of each row, overlapped with the counting — so there is no
- *    separate full-width H2D copy; pageable rows (and every row when the
- *    shape needs the global-memory kernel) are copied to device staging first;
+ *    separate full-width H2D copy; when every token array is pageable, a pool
+ *    of host threads copies the valid prefixes into library-owned pinned
+ *    memory (int64 IDs narrowed to int32 when every valid ID fits, exactly as
+ *    if the caller had passed int32) and the kernel reads those; other
+ *    pageable rows (and every row when the shape needs the global-memory
+ *    kernel) are copied whole to device staging first;
  *  - every non-NULL output is a HOST array; the kernel writes results into a
  *    pinned staging area that is copied out after the stream synchronises;
  *  - the workspace and staging buffers are owned by the library (cached per

@@ -50,6 +50,15 @@
 #include <cstring>
 #include <type_traits>
 
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
 #define TB_VERSION_STRING "tensorbleu-b200 0.1.0 (sm_100a)"
 
 namespace {
@@ -3322,6 +3331,9 @@ struct HostCtx {
   size_t pin_bytes = 0;
   unsigned char* dstage = nullptr;  // device staging for rows the kernel cannot read in place
   size_t dstage_bytes = 0;
+  unsigned char* rows = nullptr;   // pinned, mapped: valid prefixes of pageable rows
+  unsigned char* rows_dev = nullptr;
+  size_t rows_bytes = 0;
 };
 thread_local HostCtx g_host[64];
 
@@ -3351,6 +3363,174 @@ int grow_pinned(HostCtx& c, size_t want) {
   c.pin_dev = static_cast<unsigned char*>(d);
   c.pin_bytes = sz;
   return TB_OK;
+}
+
+int grow_pinned_rows(HostCtx& c, size_t want) {
+  if (c.rows_bytes >= want && c.rows) return TB_OK;
+  if (c.rows) TB_CUDA(cudaFreeHost(c.rows));
+  c.rows = nullptr;
+  c.rows_bytes = 0;
+  const size_t sz = want < (size_t(1) << 20) ? (size_t(1) << 20) : want + want / 4;
+  void* h = nullptr;
+  TB_CUDA(cudaHostAlloc(&h, sz, cudaHostAllocMapped | cudaHostAllocPortable));
+  void* dv = nullptr;
+  TB_CUDA(cudaHostGetDevicePointer(&dv, h, 0));
+  c.rows = static_cast<unsigned char*>(h);
+  c.rows_dev = static_cast<unsigned char*>(dv);
+  c.rows_bytes = sz;
+  return TB_OK;
+}
+
+// A small persistent pool of host threads for the pageable-row staging copy
+// (the caller works too).  Jobs are serialised; run(n, f) calls f(i) for
+// every i in [0, n) and returns when all are done.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  template <typename F>
+  void run(int n, F f) {
+    std::lock_guard<std::mutex> job_lock(job_);
+    std::function<void(int)> fn(f);
+    {
+      std::lock_guard<std::mutex> l(m_);
+      fn_.store(&fn);
+      n_.store(n);
+      left_.store(n);
+      next_.store(0);
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    work();
+    while (left_.load(std::memory_order_acquire) > 0) std::this_thread::yield();
+    std::lock_guard<std::mutex> l(m_);
+    fn_.store(nullptr);
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nt = std::max(0, std::min(7, static_cast<int>(hw / 2) - 1));
+    for (int i = 0; i < nt; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> l(m_);
+      stop_ = true;
+      stop_flag_.store(true);
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  void work() {
+    for (int i; (i = next_.fetch_add(1)) < n_.load();) {
+      (*fn_.load())(i);
+      left_.fetch_sub(1, std::memory_order_release);
+    }
+  }
+  void loop() {
+    unsigned seen = 0;
+    while (true) {
+      // spin briefly for the next job (calls usually come back to back; a
+      // condition-variable wake-up costs tens of microseconds), then sleep
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load() == seen && !stop_flag_.load() &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(300)) {
+      }
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return stop_ || (gen_.load() != seen && fn_.load() != nullptr); });
+        if (stop_) return;
+        seen = gen_.load();
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex job_, m_;
+  std::condition_variable cv_;
+  std::atomic<std::function<void(int)>*> fn_{nullptr};
+  std::atomic<int> n_{0};
+  std::atomic<unsigned> gen_{0};
+  bool stop_ = false;
+  std::atomic<bool> stop_flag_{false};
+  std::atomic<int> next_{1 << 30}, left_{0};
+};
+
+// Valid prefixes of pageable token rows -> pinned, mapped memory the kernel
+// reads over PCIe (instead of DMA-ing whole rows through the driver's bounce
+// buffer).  int64 rows are narrowed to int32 when every valid ID fits (the
+// common case: vocabulary IDs), halving the PCIe bytes; an ID >= 2^31 makes
+// the copy redo in int64.  Rows are written at a 16-byte-aligned stride; only
+// the clamped valid prefix of each row is written (the kernel reads no more).
+// Returns the token bytes of the staged rows (0: not staged).
+int stage_pageable_rows(HostCtx& c, int token_bytes, int nsets, const void* const* ids, const int64_t* lds,
+                        const int64_t* widths, const int64_t* const* lens, int64_t B, const void** out_ids,
+                        int64_t* out_lds, int* rc_out) {
+  *rc_out = TB_OK;
+  // the outputs may alias the inputs: keep the source pointers and strides
+  const void* src_ids[TB_MAX_REFS + 1];
+  int64_t src_lds[TB_MAX_REFS + 1];
+  for (int s = 0; s < nsets; ++s) {
+    src_ids[s] = ids[s];
+    src_lds[s] = lds[s];
+  }
+  constexpr int64_t kRowsPerItem = 16;
+  const int64_t items_per_set = (B + kRowsPerItem - 1) / kRowsPerItem;
+  auto layout = [&](int ob, size_t* offs) {
+    size_t o = 0;
+    for (int s = 0; s < nsets; ++s) {
+      offs[s] = o;
+      const int64_t ld = (widths[s] * ob + 15) / 16 * 16 / ob;
+      out_lds[s] = ld > 0 ? ld : 16 / ob;
+      o += static_cast<size_t>(B * out_lds[s] * ob + 15) / 16 * 16;
+    }
+    return o;
+  };
+  size_t offs[TB_MAX_REFS + 1];
+  for (int pass = 0; pass < 2; ++pass) {
+    const int ob = (pass == 0 && token_bytes == 8) ? 4 : token_bytes;
+    if (pass == 1 && ob == token_bytes && token_bytes == 4) break;
+    const size_t total = layout(ob, offs);
+    const int rc = grow_pinned_rows(c, total);
+    if (rc != TB_OK) {
+      *rc_out = rc;
+      return 0;
+    }
+    std::atomic<uint64_t> high{0};
+    CopyPool::get().run(static_cast<int>(items_per_set * nsets), [&](int item) {
+      const int s = static_cast<int>(item / items_per_set);
+      const int64_t b0 = (item % items_per_set) * kRowsPerItem;
+      const int64_t b1 = std::min(B, b0 + kRowsPerItem);
+      unsigned char* dst = c.rows + offs[s];
+      uint64_t hi = 0;
+      for (int64_t b = b0; b < b1; ++b) {
+        int64_t n = lens[s][b];
+        n = n < 0 ? 0 : (n > widths[s] ? widths[s] : n);  // the kernel's clamp (it flags the row)
+        if (token_bytes == 8 && ob == 4) {
+          const int64_t* src = static_cast<const int64_t*>(src_ids[s]) + b * src_lds[s];
+          int32_t* o = reinterpret_cast<int32_t*>(dst) + b * out_lds[s];
+          for (int64_t j = 0; j < n; ++j) {
+            const int64_t v = src[j];
+            hi |= static_cast<uint64_t>(v) >> 31;
+            o[j] = static_cast<int32_t>(v);
+          }
+        } else if (n > 0) {
+          memcpy(dst + static_cast<size_t>(b * out_lds[s]) * ob,
+                 static_cast<const unsigned char*>(src_ids[s]) + static_cast<size_t>(b * src_lds[s]) * token_bytes,
+                 static_cast<size_t>(n) * token_bytes);
+        }
+      }
+      if (hi) high.fetch_or(hi, std::memory_order_relaxed);
+    });
+    if (ob == token_bytes || high.load() == 0) {
+      for (int s = 0; s < nsets; ++s) out_ids[s] = c.rows + offs[s];
+      return ob;
+    }
+  }
+  return 0;
 }
 
 enum Where { kDeviceMem = 0, kPinnedHost = 1, kPageableHost = 2 };
@@ -3460,28 +3640,7 @@ int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int
   DevInfo* d = nullptr;
   rc = dev_info(&d);
   if (rc != TB_OK) return rc;
-  Plan pl;
-  if (batch > 0) {
-    rc = make_plan(batch, R, cand_width, ref_width, token_bytes, N, d->smem_optin, d->sms, &pl);
-    if (rc != TB_OK) return rc;
-  }
-  rc = grow_device(&c.ws, &c.ws_bytes, pl.ws_bytes > kAccBytes ? pl.ws_bytes : kAccBytes, true);
-  if (rc != TB_OK) return rc;
-
-  // ---- pinned staging layout: [err | outputs | pageable lengths]
   const int64_t B = batch;
-  struct Out { void* user; size_t bytes; size_t off; };
-  Out outs[9] = {{num_out, size_t(B * N) * 8, 0},   {den_out, size_t(B * N) * 8, 0},
-                 {cand_len_out, size_t(B) * 8, 0},  {eff_ref_out, size_t(B) * 8, 0},
-                 {scores_out, size_t(B) * 8, 0},    {precisions_out, size_t(B * N) * 8, 0},
-                 {bp_out, size_t(B) * 8, 0},        {totals_out, size_t(2 * N + 2) * 8, 0},
-                 {corpus_out, size_t(N + 2) * 8, 0}};
-  size_t off = 256;  // err word
-  for (auto& o : outs)
-    if (o.user) {
-      o.off = off;
-      off = align_up(off + o.bytes);
-    }
   const void* ids_in[TB_MAX_REFS + 1];
   const int64_t* len_in[TB_MAX_REFS + 1];
   int64_t lds[TB_MAX_REFS + 1], widths[TB_MAX_REFS + 1];
@@ -3495,6 +3654,50 @@ int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int
     lds[r + 1] = ref_ld[r];
     widths[r + 1] = ref_width[r];
   }
+  // Pageable token rows (e.g. numpy arrays): copy their valid prefixes into
+  // pinned memory with the host thread pool — narrowed to int32 when every ID
+  // fits — for the kernel to read over PCIe, when the shared-memory kernels
+  // take the rows (they stage valid prefixes).  Otherwise the rows are DMA'd
+  // whole below.
+  // (Pinned rows are read in place: staging pinned int64 rows to narrow them
+  // lost on cold data — the copy reads 8 bytes per token from DRAM.)
+  if (B > 0) {
+    bool pageable = true;
+    for (int s = 0; s <= R && pageable; ++s) {
+      const void* v = nullptr;
+      if (classify(len_in[s], &v) == kDeviceMem) pageable = false;
+      if (widths[s] > 0 && classify(ids_in[s], &v) != kPageableHost) pageable = false;
+    }
+    Plan probe;
+    if (pageable && make_plan(B, R, cand_width, ref_width, 4, N, d->smem_optin, d->sms, &probe) == TB_OK &&
+        probe.smem_mode) {
+      int src = TB_OK;
+      const int tb = stage_pageable_rows(c, token_bytes, R + 1, ids_in, lds, widths, len_in, B, ids_in, lds, &src);
+      if (src != TB_OK) return src;
+      if (tb) token_bytes = tb;
+    }
+  }
+  Plan pl;
+  if (batch > 0) {
+    rc = make_plan(batch, R, cand_width, ref_width, token_bytes, N, d->smem_optin, d->sms, &pl);
+    if (rc != TB_OK) return rc;
+  }
+  rc = grow_device(&c.ws, &c.ws_bytes, pl.ws_bytes > kAccBytes ? pl.ws_bytes : kAccBytes, true);
+  if (rc != TB_OK) return rc;
+
+  // ---- pinned staging layout: [err | outputs | pageable lengths]
+  struct Out { void* user; size_t bytes; size_t off; };
+  Out outs[9] = {{num_out, size_t(B * N) * 8, 0},   {den_out, size_t(B * N) * 8, 0},
+                 {cand_len_out, size_t(B) * 8, 0},  {eff_ref_out, size_t(B) * 8, 0},
+                 {scores_out, size_t(B) * 8, 0},    {precisions_out, size_t(B * N) * 8, 0},
+                 {bp_out, size_t(B) * 8, 0},        {totals_out, size_t(2 * N + 2) * 8, 0},
+                 {corpus_out, size_t(N + 2) * 8, 0}};
+  size_t off = 256;  // err word
+  for (auto& o : outs)
+    if (o.user) {
+      o.off = off;
+      off = align_up(off + o.bytes);
+    }
   const void* ids_dev[TB_MAX_REFS + 1];
   const int64_t* len_dev[TB_MAX_REFS + 1];
   Where len_where[TB_MAX_REFS + 1];
@@ -3548,7 +3751,7 @@ int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int
   auto P = [&](int i) -> void* { return outs[i].user ? c.pin_dev + outs[i].off : nullptr; };
   int32_t* err_host = reinterpret_cast<int32_t*>(c.pin);
   *err_host = 0;
-  rc = stats_impl(token_bytes, ids_dev[0], cand_ld, cand_width, len_dev[0], R, ids_dev + 1, ref_ld, ref_width,
+  rc = stats_impl(token_bytes, ids_dev[0], lds[0], cand_width, len_dev[0], R, ids_dev + 1, lds + 1, ref_width,
                   len_dev + 1, B, N, smoothing, eps, k, weights, static_cast<int64_t*>(P(0)),
                   static_cast<int64_t*>(P(1)), static_cast<int64_t*>(P(2)), static_cast<int64_t*>(P(3)),
                   static_cast<double*>(P(4)), static_cast<double*>(P(5)), static_cast<double*>(P(6)),

@@ -5,7 +5,8 @@
 Draws random shapes (batch, row widths per reference set, 1..12 references),
 vocabularies (1 .. 2^40), token dtypes, max orders (1..9), mutation rates
 (related and unrelated text) and lengths (including 0 and the full width),
-runs compute_stats on CUDA tensors and on pinned host tensors, and asserts the
+runs compute_stats on CUDA tensors, pinned host tensors, pageable numpy arrays
+and pageable torch tensors, and asserts the
 counts are bit-identical to the oracle and the fp64 scores (smoothing cycling
 through none / floor / add-k / exp) agree within 1e-12 relative with the
 same zero set.  Prints the first failing case with
@@ -56,6 +57,10 @@ def run(cid, clen, refs, n, dt, where, smoothing="none"):
     if where == "cuda":
         mk = lambda i, ln: tb.TokenBatch(ids=torch.as_tensor(i).to(dt).cuda(),  # noqa: E731
                                          lengths=torch.as_tensor(ln).cuda())
+    elif where == "numpy":  # pageable host arrays, the reference's TokenBatch usage
+        mk = lambda i, ln: tb.TokenBatch(ids=i, lengths=ln)  # noqa: E731
+    elif where == "pageable":  # pageable torch tensors of the token dtype
+        mk = lambda i, ln: tb.TokenBatch(ids=torch.as_tensor(i).to(dt), lengths=torch.as_tensor(ln))  # noqa: E731
     else:
         mk = lambda i, ln: tb.TokenBatch(ids=torch.as_tensor(i).to(dt).pin_memory(),  # noqa: E731
                                          lengths=torch.as_tensor(ln))
@@ -81,7 +86,7 @@ def main():
         o = oracle.stats(cid, clen, refs, n)
         sm = ("none", "floor", "add-k", "exp")[k % 4]
         os_ = oracle.scores(o, sm)["scores"]
-        for where in ("cuda", "host"):
+        for where in ("cuda", "host", "numpy", "pageable"):
             num, den, eff, sc = run(cid, clen, refs, n, dt, where, sm)
             ok = (np.array_equal(num, o["numerators"]) and np.array_equal(den, o["denominators"])
                   and np.array_equal(eff, o["eff_ref_lens"])
@@ -94,7 +99,7 @@ def main():
                       f"max score rel err {np.max(np.abs(sc - os_) / np.maximum(np.abs(os_), 1e-300)):.3g}")
                 sys.exit(1)
         k += 1
-    print(f"fuzz ok: {k} cases x 2 paths in {time.time() - t0:.0f} s")
+    print(f"fuzz ok: {k} cases x 4 paths in {time.time() - t0:.0f} s")
 
 
 if __name__ == "__main__":
