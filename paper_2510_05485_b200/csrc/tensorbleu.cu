@@ -3459,6 +3459,43 @@ class CopyPool {
   std::atomic<int> next_{1 << 30}, left_{0};
 };
 
+// Copy the clamped valid prefixes of rows [b0, b1) of every set to dst[s]
+// (row stride dst_lds[s] elements of `ob` bytes; int64 -> int32 when ob == 4
+// < token_bytes) on the host thread pool.  Returns the OR of the bits of the
+// narrowed IDs above bit 30 (non-zero: some ID does not fit int32).
+uint64_t copy_rows(int token_bytes, int ob, int nsets, const void* const* ids, const int64_t* lds,
+                   const int64_t* widths, const int64_t* const* lens, int64_t b0, int64_t b1,
+                   unsigned char* const* dst, const int64_t* dst_lds) {
+  constexpr int64_t kRowsPerItem = 16;
+  const int64_t per_set = (b1 - b0 + kRowsPerItem - 1) / kRowsPerItem;
+  std::atomic<uint64_t> high{0};
+  CopyPool::get().run(static_cast<int>(per_set * nsets), [&](int item) {
+    const int s = static_cast<int>(item / per_set);
+    const int64_t r0 = b0 + (item % per_set) * kRowsPerItem;
+    const int64_t r1 = std::min(b1, r0 + kRowsPerItem);
+    uint64_t hi = 0;
+    for (int64_t b = r0; b < r1; ++b) {
+      int64_t n = lens[s][b];
+      n = n < 0 ? 0 : (n > widths[s] ? widths[s] : n);  // the kernel's clamp (it flags the row)
+      unsigned char* o = dst[s] + static_cast<size_t>((b - b0) * dst_lds[s]) * ob;
+      if (token_bytes == 8 && ob == 4) {
+        const int64_t* src = static_cast<const int64_t*>(ids[s]) + b * lds[s];
+        int32_t* o32 = reinterpret_cast<int32_t*>(o);
+        for (int64_t j = 0; j < n; ++j) {
+          const int64_t v = src[j];
+          hi |= static_cast<uint64_t>(v) >> 31;
+          o32[j] = static_cast<int32_t>(v);
+        }
+      } else if (n > 0) {
+        memcpy(o, static_cast<const unsigned char*>(ids[s]) + static_cast<size_t>(b * lds[s]) * token_bytes,
+               static_cast<size_t>(n) * token_bytes);
+      }
+    }
+    if (hi) high.fetch_or(hi, std::memory_order_relaxed);
+  });
+  return high.load();
+}
+
 // Valid prefixes of pageable token rows -> pinned, mapped memory the kernel
 // reads over PCIe (instead of DMA-ing whole rows through the driver's bounce
 // buffer).  int64 rows are narrowed to int32 when every valid ID fits (the
@@ -3611,6 +3648,110 @@ int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, in
                     workspace_bytes, stream, 0, 0);
 }
 
+// Pageable rows, per-sentence outputs, B >= 2 * kPipeRows: the batch runs in
+// chunks of rows — the host threads stage chunk i + 1 (valid prefixes, int64
+// narrowed to int32 when its IDs fit) while the kernel reads chunk i over
+// PCIe — one launch per chunk on `stream`, one synchronisation at the end.
+constexpr int64_t kPipeRows = 512;
+constexpr int kPipeMaxChunks = 8;
+int host_pipelined(HostCtx& c, int token_bytes, int R, const void* const* ids, const int64_t* lds,
+                   const int64_t* widths, const int64_t* const* lens, int64_t B, int N, int smoothing, double eps,
+                   double k, const double* weights, int64_t* num_out, int64_t* den_out, int64_t* cand_len_out,
+                   int64_t* eff_ref_out, double* scores_out, double* precisions_out, double* bp_out,
+                   int32_t* flags_out, cudaStream_t stream) {
+  const int nsets = R + 1;
+  int nchunks = static_cast<int>(B / kPipeRows);
+  nchunks = nchunks < kPipeMaxChunks ? nchunks : kPipeMaxChunks;
+  const int64_t rows_per = (B + nchunks - 1) / nchunks;
+  // pinned staging: [err word per chunk | outputs | pageable lengths]
+  struct Out { void* user; size_t bytes; size_t off; int64_t per_row; };
+  Out outs[7] = {{num_out, size_t(B * N) * 8, 0, N},  {den_out, size_t(B * N) * 8, 0, N},
+                 {cand_len_out, size_t(B) * 8, 0, 1}, {eff_ref_out, size_t(B) * 8, 0, 1},
+                 {scores_out, size_t(B) * 8, 0, 1},   {precisions_out, size_t(B * N) * 8, 0, N},
+                 {bp_out, size_t(B) * 8, 0, 1}};
+  size_t off = 256;  // kPipeMaxChunks err words
+  for (auto& o : outs)
+    if (o.user) {
+      o.off = off;
+      off = align_up(off + o.bytes);
+    }
+  const void* v = nullptr;
+  size_t len_off[TB_MAX_REFS + 1];
+  const int64_t* len_dev[TB_MAX_REFS + 1];
+  for (int s = 0; s < nsets; ++s) {
+    len_dev[s] = nullptr;
+    len_off[s] = 0;
+    if (classify(lens[s], &v) == kPageableHost) {
+      len_off[s] = off;
+      off = align_up(off + size_t(B) * 8);
+    } else {
+      len_dev[s] = static_cast<const int64_t*>(v);  // pinned: its device view
+    }
+  }
+  int rc = grow_pinned(c, off);
+  if (rc != TB_OK) return rc;
+  for (int s = 0; s < nsets; ++s)
+    if (!len_dev[s]) {
+      memcpy(c.pin + len_off[s], lens[s], size_t(B) * 8);
+      len_dev[s] = reinterpret_cast<const int64_t*>(c.pin_dev + len_off[s]);
+    }
+  // rows: one region per (chunk, set), sized for int64 rows
+  int64_t ld4[TB_MAX_REFS + 1], ld8[TB_MAX_REFS + 1];
+  size_t region[TB_MAX_REFS + 1], chunk_bytes = 0;
+  for (int s = 0; s < nsets; ++s) {
+    ld4[s] = widths[s] > 0 ? (widths[s] + 3) / 4 * 4 : 4;
+    ld8[s] = widths[s] > 0 ? (widths[s] + 1) / 2 * 2 : 2;
+    const size_t a = size_t(rows_per * ld4[s]) * 4, b8 = size_t(rows_per * ld8[s]) * 8;
+    region[s] = align_up(a > b8 ? a : b8);
+    chunk_bytes += region[s];
+  }
+  rc = grow_pinned_rows(c, chunk_bytes * nchunks);
+  if (rc != TB_OK) return rc;
+  rc = grow_device(&c.ws, &c.ws_bytes, kAccBytes, true);  // the shared-memory plans need the completion region only
+  if (rc != TB_OK) return rc;
+  int32_t* err_host = reinterpret_cast<int32_t*>(c.pin);
+  for (int i = 0; i < nchunks; ++i) err_host[i] = 0;
+  auto P = [&](int i, int64_t b0) -> void* {
+    return outs[i].user ? c.pin_dev + outs[i].off + size_t(b0 * outs[i].per_row) * 8 : nullptr;
+  };
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int64_t b0 = ci * rows_per;
+    const int64_t b1 = b0 + rows_per < B ? b0 + rows_per : B;
+    if (b1 <= b0) break;
+    unsigned char* dst[TB_MAX_REFS + 1];
+    const void* dev_ids[TB_MAX_REFS + 1];
+    size_t o = chunk_bytes * ci;
+    for (int s = 0; s < nsets; ++s) {
+      dst[s] = c.rows + o;
+      dev_ids[s] = c.rows_dev + o;
+      o += region[s];
+    }
+    int ob = token_bytes == 8 ? 4 : token_bytes;
+    const int64_t* dlds = ob == 4 ? ld4 : ld8;
+    if (copy_rows(token_bytes, ob, nsets, ids, lds, widths, lens, b0, b1, dst, dlds) != 0) {
+      ob = 8;  // an ID >= 2^31 in this chunk: stage it as int64
+      dlds = ld8;
+      copy_rows(token_bytes, ob, nsets, ids, lds, widths, lens, b0, b1, dst, dlds);
+    }
+    const int64_t* lchunk[TB_MAX_REFS + 1];
+    for (int s = 0; s < nsets; ++s) lchunk[s] = len_dev[s] + b0;
+    rc = stats_impl(ob, dev_ids[0], dlds[0], widths[0], lchunk[0], R, dev_ids + 1, dlds + 1, widths + 1, lchunk + 1,
+                    b1 - b0, N, smoothing, eps, k, weights, static_cast<int64_t*>(P(0, b0)),
+                    static_cast<int64_t*>(P(1, b0)), static_cast<int64_t*>(P(2, b0)),
+                    static_cast<int64_t*>(P(3, b0)), static_cast<double*>(P(4, b0)),
+                    static_cast<double*>(P(5, b0)), static_cast<double*>(P(6, b0)), nullptr, nullptr,
+                    reinterpret_cast<int32_t*>(c.pin_dev) + ci, c.ws, c.ws_bytes, stream, 1, 1);
+    if (rc != TB_OK) return rc;
+  }
+  TB_CUDA(cudaStreamSynchronize(stream));
+  for (auto& ou : outs)
+    if (ou.user && ou.bytes) memcpy(ou.user, c.pin + ou.off, ou.bytes);
+  int32_t flags = 0;
+  for (int i = 0; i < nchunks; ++i) flags |= reinterpret_cast<volatile int32_t*>(err_host)[i];
+  *flags_out = flags;
+  return TB_OK;
+}
+
 int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int64_t cand_width,
                  const int64_t* cand_len, int32_t num_refs, const void* const* ref_ids,
                  const int64_t* ref_ld, const int64_t* ref_width, const int64_t* const* ref_len,
@@ -3668,7 +3809,16 @@ int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int
       if (classify(len_in[s], &v) == kDeviceMem) pageable = false;
       if (widths[s] > 0 && classify(ids_in[s], &v) != kPageableHost) pageable = false;
     }
-    Plan probe;
+    Plan probe, probe8;
+    const bool corpus_mode = totals_out != nullptr || corpus_out != nullptr;
+    if (pageable && !corpus_mode && B >= 2 * kPipeRows &&
+        make_plan(kPipeRows, R, cand_width, ref_width, 4, N, d->smem_optin, d->sms, &probe) == TB_OK &&
+        probe.smem_mode &&
+        make_plan(kPipeRows, R, cand_width, ref_width, 8, N, d->smem_optin, d->sms, &probe8) == TB_OK &&
+        probe8.smem_mode)
+      return host_pipelined(c, token_bytes, R, ids_in, lds, widths, len_in, B, N, smoothing, eps, k, weights,
+                            num_out, den_out, cand_len_out, eff_ref_out, scores_out, precisions_out, bp_out,
+                            flags_out, stream);
     if (pageable && make_plan(B, R, cand_width, ref_width, 4, N, d->smem_optin, d->sms, &probe) == TB_OK &&
         probe.smem_mode) {
       int src = TB_OK;
