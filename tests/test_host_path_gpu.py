@@ -166,3 +166,44 @@ def test_bad_lengths_are_flagged(where):
     assert f & _native.TB_FLAG_BAD_LENGTH
     f, _ = _raw_host_call(ids, lens, ids, lens)  # flags do not stick
     assert f == 0
+
+
+@pytest.mark.parametrize("R", [1, 3])
+def test_pageable_numpy_rows_staged_and_pipelined(R):
+    """numpy (pageable) rows — the reference's own TokenBatch usage — are staged
+    into pinned memory by host threads, narrowed to int32 when their IDs fit;
+    batches of >= 1024 rows run in chunks (copy of chunk i+1 overlapping the
+    kernel on chunk i), and a chunk holding an ID >= 2^31 is staged as int64."""
+    rng = np.random.default_rng(500 + R)
+    (cid, clen), refs = _correlated(rng, 1100, 96, 3000, R)
+    cid[700, 5] = 2 ** 40          # only the second chunk needs int64
+    refs[0][0][700, 5] = 2 ** 40
+    clen[1000] = 0
+    cand = tb.TokenBatch(ids=cid, lengths=clen)
+    rb = [tb.TokenBatch(ids=i, lengths=l) for i, l in refs]
+    st = tb.compute_stats(cand, rb, tb.BleuConfig(smoothing="floor"))
+    o = oracle.stats(cid, clen, refs, 4)
+    np.testing.assert_array_equal(st.numerators, o["numerators"])
+    np.testing.assert_array_equal(st.denominators, o["denominators"])
+    np.testing.assert_array_equal(st.eff_ref_lens, o["eff_ref_lens"])
+    res = tb.sentence_bleu(cand, rb, tb.BleuConfig(smoothing="floor"))
+    os_ = oracle.scores(o, "floor")
+    np.testing.assert_allclose(res.scores, os_["scores"], rtol=RTOL, atol=0)
+    np.testing.assert_allclose(res.precisions, os_["precisions"], rtol=RTOL, atol=0)
+    # the same rows, small batch (one staged launch) and pinned (read in place)
+    small = tb.TokenBatch(ids=cid[:200], lengths=clen[:200])
+    rs = [tb.TokenBatch(ids=i[:200], lengths=l[:200]) for i, l in refs]
+    np.testing.assert_array_equal(tb.compute_stats(small, rs, tb.BleuConfig()).numerators, o["numerators"][:200])
+
+
+def test_pageable_bad_lengths_flagged_in_pipelined_chunks():
+    rng = np.random.default_rng(9)
+    ids = rng.integers(0, 50, (1100, 40))
+    lens = np.full(1100, 40)
+    bad = lens.copy()
+    bad[900] = 41  # in the second chunk
+    f, num = _raw_host_call(torch.as_tensor(ids), torch.as_tensor(bad), torch.as_tensor(ids), torch.as_tensor(lens))
+    assert f & _native.TB_FLAG_BAD_LENGTH
+    f, num = _raw_host_call(torch.as_tensor(ids), torch.as_tensor(lens), torch.as_tensor(ids), torch.as_tensor(lens))
+    assert f == 0
+    np.testing.assert_array_equal(num[:, 0], 40)
