@@ -28,7 +28,7 @@ import paper_2510_05485_b200 as tb  # noqa: E402
 
 
 def case(rng):
-    b = int(rng.choice([1, 3, 17, 64, 700]))
+    b = int(rng.choice([1, 3, 17, 64, 700, 1100]))
     R = int(rng.choice([1, 1, 1, 2, 3, 4, 8, 12]))
     lc = int(rng.choice([1, 7, 64, 300, 1024, 2048]))
     v = int(rng.choice([1, 3, 50, 2000, 128000, 2 ** 40]))
