@@ -3383,7 +3383,9 @@ int grow_pinned_rows(HostCtx& c, size_t want) {
 
 // A small persistent pool of host threads for the pageable-row staging copy
 // (the caller works too).  Jobs are serialised; run(n, f) calls f(i) for
-// every i in [0, n) and returns when all are done.
+// every i in [0, n) exactly once and returns when all are done.  Work items
+// are claimed by CAS on a counter tagged with the job number, so a worker that
+// is late for one job can never claim (or skip) an item of the next one.
 class CopyPool {
  public:
   static CopyPool& get() {
@@ -3394,19 +3396,19 @@ class CopyPool {
   void run(int n, F f) {
     std::lock_guard<std::mutex> job_lock(job_);
     std::function<void(int)> fn(f);
+    uint32_t g;
     {
       std::lock_guard<std::mutex> l(m_);
-      fn_.store(&fn);
-      n_.store(n);
+      g = ++gen_;
+      fn_ = &fn;
+      n_ = n;
       left_.store(n);
-      next_.store(0);
-      gen_.fetch_add(1);
+      next_.store(static_cast<uint64_t>(g) << 32);
+      gen_pub_.store(g);
     }
     cv_.notify_all();
-    work();
+    work(g, &fn, n);
     while (left_.load(std::memory_order_acquire) > 0) std::this_thread::yield();
-    std::lock_guard<std::mutex> l(m_);
-    fn_.store(nullptr);
   }
 
  private:
@@ -3419,44 +3421,57 @@ class CopyPool {
     {
       std::lock_guard<std::mutex> l(m_);
       stop_ = true;
-      stop_flag_.store(true);
     }
+    stop_flag_.store(true);
     cv_.notify_all();
     for (auto& t : threads_) t.join();
   }
-  void work() {
-    for (int i; (i = next_.fetch_add(1)) < n_.load();) {
-      (*fn_.load())(i);
+  // claim items of job g only (never touches another job's counter)
+  void work(uint32_t g, std::function<void(int)>* fn, int n) {
+    uint64_t v = next_.load();
+    while (true) {
+      if (static_cast<uint32_t>(v >> 32) != g || static_cast<int>(v & 0xffffffffu) >= n) return;
+      if (!next_.compare_exchange_weak(v, v + 1)) continue;
+      (*fn)(static_cast<int>(v & 0xffffffffu));
       left_.fetch_sub(1, std::memory_order_release);
+      v = next_.load();
     }
   }
   void loop() {
-    unsigned seen = 0;
+    uint32_t seen = 0;
     while (true) {
       // spin briefly for the next job (calls usually come back to back; a
       // condition-variable wake-up costs tens of microseconds), then sleep
       const auto t0 = std::chrono::steady_clock::now();
-      while (gen_.load() == seen && !stop_flag_.load() &&
+      while (gen_pub_.load() == seen && !stop_flag_.load() &&
              std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(300)) {
       }
+      uint32_t g;
+      std::function<void(int)>* fn;
+      int n;
       {
         std::unique_lock<std::mutex> l(m_);
-        cv_.wait(l, [&] { return stop_ || (gen_.load() != seen && fn_.load() != nullptr); });
+        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
         if (stop_) return;
-        seen = gen_.load();
+        g = seen = gen_;
+        fn = fn_;
+        n = n_;
       }
-      work();
+      work(g, fn, n);
     }
   }
   std::vector<std::thread> threads_;
   std::mutex job_, m_;
   std::condition_variable cv_;
-  std::atomic<std::function<void(int)>*> fn_{nullptr};
-  std::atomic<int> n_{0};
-  std::atomic<unsigned> gen_{0};
+  // the current job (written under m_)
+  uint32_t gen_ = 0;
+  std::function<void(int)>* fn_ = nullptr;
+  int n_ = 0;
   bool stop_ = false;
+  std::atomic<uint32_t> gen_pub_{0};
   std::atomic<bool> stop_flag_{false};
-  std::atomic<int> next_{1 << 30}, left_{0};
+  std::atomic<uint64_t> next_{0};
+  std::atomic<int> left_{0};
 };
 
 // Copy the clamped valid prefixes of rows [b0, b1) of every set to dst[s]
