@@ -49,6 +49,13 @@ def main():
         tb.corpus_bleu(cand, refs)
         if c.get("corr"):  # long orders: list rounds beyond order 4, warp-path hand-over
             tb.sentence_bleu(cand, refs, tb.BleuConfig(max_order=9, smoothing="floor"))
+    # pageable numpy rows: staged into pinned memory (narrowed), chunk-pipelined for >= 1024 rows
+    for bsz in (300, 1100):
+        cid = rng.integers(0, 5000, (bsz, 64))
+        cl = rng.integers(0, 65, bsz)
+        rid = np.where(rng.random((bsz, 64)) < 0.5, cid, rng.integers(0, 5000, (bsz, 64)))
+        tb.sentence_bleu(tb.TokenBatch(ids=cid, lengths=cl), [tb.TokenBatch(ids=rid, lengths=cl)],
+                         tb.BleuConfig(smoothing="floor"))
     d = torch.device("cuda", 0)
     cand, refs = batch(rng, 64, 128, 500, 1, dev=d)
     tb.compute_stats(cand, refs, tb.BleuConfig())
