@@ -140,7 +140,7 @@ int tb_bleu_stats(int32_t token_bytes,
  *    of host threads copies the valid prefixes into library-owned pinned
  *    memory (int64 IDs narrowed to int32 when every valid ID fits, exactly as
  *    if the caller had passed int32) and the kernel reads those (batches of
- *    >= 512 rows with per-sentence outputs in chunks: one launch per chunk,
+ *    >= 1024 rows with per-sentence outputs in chunks: one launch per chunk,
  *    the copy of the next chunk overlapping the kernel on this one); other
  *    pageable rows (and every row when the shape needs the global-memory
  *    kernel) are copied whole to device staging first;

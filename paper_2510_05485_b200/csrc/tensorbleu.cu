@@ -3667,7 +3667,7 @@ int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, in
 // chunks of rows — the host threads stage chunk i + 1 (valid prefixes, int64
 // narrowed to int32 when its IDs fit) while the kernel reads chunk i over
 // PCIe — one launch per chunk on `stream`, one synchronisation at the end.
-constexpr int64_t kPipeRows = 256;
+constexpr int64_t kPipeRows = 512;
 constexpr int kPipeMaxChunks = 8;
 int host_pipelined(HostCtx& c, int token_bytes, int R, const void* const* ids, const int64_t* lds,
                    const int64_t* widths, const int64_t* const* lens, int64_t B, int N, int smoothing, double eps,

@@ -172,7 +172,7 @@ def test_bad_lengths_are_flagged(where):
 def test_pageable_numpy_rows_staged_and_pipelined(R):
     """numpy (pageable) rows — the reference's own TokenBatch usage — are staged
     into pinned memory by host threads, narrowed to int32 when their IDs fit;
-    batches of >= 512 rows run in chunks (copy of chunk i+1 overlapping the
+    batches of >= 1024 rows run in chunks (copy of chunk i+1 overlapping the
     kernel on chunk i), and a chunk holding an ID >= 2^31 is staged as int64."""
     rng = np.random.default_rng(500 + R)
     (cid, clen), refs = _correlated(rng, 1100, 96, 3000, R)
