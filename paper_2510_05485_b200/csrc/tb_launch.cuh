@@ -1,0 +1,88 @@
+// tb_launch.cuh — shape plan + launch helper shared by the kernel translation
+// units and the runtime (tb_runtime.cu).
+#pragma once
+
+#include "tb_common.cuh"
+
+namespace tbk {
+
+// --------------------------------------------------------------------------
+// Shape planning shared by the workspace query and the launch.
+// --------------------------------------------------------------------------
+struct Plan {
+  bool smem_mode = false;
+  bool pair = false;   // single-reference kernel
+  bool multi = false;  // multi-reference kernel
+  int cap_log2 = 0;
+  int filter_log2 = 0;
+  int cand_pad = 0;
+  int ref_off[TB_MAX_REFS + 1] = {0};
+  int off_id1 = 0, off_idn = 0, off_live = 0, off_ent = 0, off_mref = 0, off_kc = 0, off_lists = 0, off_seg = 0;
+  int off_tok2 = 0;
+  size_t smem_bytes = 0;   // dynamic smem (smem mode)
+  size_t gtab_stride = 0;  // per-CTA table bytes (global mode)
+  int64_t grid = 0;
+  size_t acc_bytes = 0;
+  size_t ws_bytes = 0;
+};
+
+constexpr size_t kStaticSmemReserve = 2048;  // static __shared__ of the stats kernels (upper bound)
+constexpr int64_t kGlobalGridCap = 2 * 148;
+// fixed-size completion region at the start of the workspace, independent of N
+constexpr size_t kAccBytes = ((kAccCopies * (2 * TB_MAX_ORDER + 2) * 8 + 256) + 255) / 256 * 256;
+
+template <typename K>
+int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool persistent_fill,
+                  size_t* attr_set, cudaStream_t stream, int threads = kThreads) {
+  int dev = 0;
+  TB_CUDA(cudaGetDevice(&dev));
+  if (pl.smem_bytes > 48 * 1024 && attr_set[dev & 63] < pl.smem_bytes) {
+    TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(pl.smem_bytes)));
+    attr_set[dev & 63] = pl.smem_bytes;
+  }
+  int64_t grid = pl.grid;
+  if (persistent_fill) {
+    // occupancy per (device, dynamic smem) of this kernel instantiation, cached:
+    // the query costs microseconds on every launch otherwise
+    static thread_local struct { int dev; size_t smem; int occ; } cache[8] = {};
+    static thread_local int next = 0;
+    int occ = 0;
+    for (auto& e : cache)
+      if (e.occ > 0 && e.dev == dev && e.smem == pl.smem_bytes) occ = e.occ;
+    if (occ == 0) {
+      TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, pl.smem_bytes));
+      if (occ < 1) occ = 1;
+      cache[next] = {dev, pl.smem_bytes, occ};
+      next = (next + 1) & 7;
+    }
+    const int64_t resident = static_cast<int64_t>(occ) * sms;
+    grid = prm.batch < resident ? prm.batch : resident;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = pl.smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TB_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+// per-kernel launchers (one translation unit each); token_bytes 4 or 8
+int launch_pair(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes);
+int launch_multi(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes);
+int launch_group(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes);
+int launch_global(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes);
+#ifdef TB_PHASES
+int set_phases_pair(void* buf);
+int set_phases_multi(void* buf);
+int set_phases_group(void* buf);
+#endif
+
+}  // namespace tbk
