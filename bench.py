@@ -1,14 +1,30 @@
 """Benchmark: per-sentence BLEU-4 sentences/s at 512x1024 tokens (V=128k, R=1),
-BASELINE.json configs[1] — plus the HBM roofline of the fused kernel and the
-reference CPU path timed on this host.
+BASELINE.json configs[1] — plus the HBM roofline of the fused kernel, the
+reference CPU path timed on this host, and every other BASELINE config in a
+``configs`` sub-object of the same JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1..c5] [--data uniform|correlated|zipf|vocab1]
+                    [--scaling weak|strong] [--no-configs]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 A "step" is one pass of the hot path over one batch of the workload: the
-batch's per-sentence statistics and BLEU scores.  Multi-GPU is weak scaling:
-every rank scores its own 512x1024 batch (rows shard with no data-path
-collective), value = all sentences / max-over-ranks time.
+batch's per-sentence statistics and BLEU scores (corpus: the int64 totals,
+their NCCL all-reduce across ranks and the corpus score).  Scaling:
+
+* weak (c1, c2, c3 — the headline c2): every rank scores its own batch of the
+  workload's shape (rows shard with no data-path collective);
+  value = all sentences / max-over-ranks time;
+* strong (c4, c5): ONE global batch (4096x1024 corpus; 16384x2048) split in
+  contiguous ceil(B/N)-row shards; c4 all-reduces the int64 totals (NCCL) and
+  runs the corpus epilogue inside the timed region.
+
+Every measured configuration is verified AFTER its timed loop: the timed
+plan is run once more on batch 0 (the reference generator's batch) and its
+counts / lengths must be bit-identical and its fp64 scores within 1e-12
+relative of the reference's own ``batchbleu`` (headline) or of the C
+restatement (other configs); a mismatch prints {"error": ...} and exits 2
+(the reference bench's equivalence gate, bench.py:104-113, 240-242).
 """
 
 from __future__ import annotations
@@ -27,25 +43,30 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# name: (B, L, V, R, smoothing, mode, default scaling) — BASELINE.json configs
 WORKLOADS = {
-    # name: (B, L, V, R, smoothing)   — BASELINE.json configs
-    "c1": (16, 256, 32000, 1, "floor"),
-    "c2": (512, 1024, 128000, 1, "none"),
-    "c3": (256, 1024, 128000, 4, "add-k"),
-    "c4": (4096, 1024, 128000, 1, "none"),
-    "c5": (2048, 2048, 256000, 1, "none"),  # per-GPU shard of 16384x2048 over 8 GPUs
+    "c1": (16, 256, 32000, 1, "floor", "sentence", "weak"),
+    "c2": (512, 1024, 128000, 1, "none", "sentence", "weak"),
+    "c3": (256, 1024, 128000, 4, "add-k", "sentence", "weak"),
+    "c4": (4096, 1024, 128000, 1, "none", "corpus", "strong"),
+    "c5": (16384, 2048, 256000, 1, "none", "sentence", "strong"),
 }
-# c4 is corpus BLEU: one score for the whole (sharded) batch, totals NCCL-all-reduced
-MODES = {"c4": "corpus"}
+# the configs sub-object of the headline line: (workload, data)
+CONFIG_GRID = [("c1", "uniform"), ("c2", "correlated"), ("c2", "zipf"), ("c2", "vocab1"),
+               ("c3", "uniform"), ("c3", "correlated"), ("c4", "uniform"), ("c4", "correlated"),
+               ("c5", "uniform"), ("c5", "correlated")]
 METRIC = "per-sentence BLEU-4 sentences/sec at 512x1024 tok; HBM roofline %; vs CPU ref"
 L2_FLUSH_BYTES = 256 << 20
+SCORE_RTOL = 1e-12  # north_star: fp64 scores within 1e-12 relative
 
 
 def generate_batch(b, l, v, r, seed=42, data="uniform"):
     """The reference generator, bench.py:72-91: default_rng([seed, B, L, V]),
     IDs uniform in [0, V), lengths uniform in [L/2, L]; candidates then refs.
-    data="correlated" (SURVEY §8d parity input): every reference is the
-    candidate with a per-row mutation rate p ~ U[0, 0.9] and length +-50."""
+    Other parity inputs of SURVEY §8d on the same lengths:
+    correlated — every reference is the candidate with a per-row mutation rate
+    p ~ U[0, 0.9] and length +-50; zipf — Zipf(1.1) token IDs (hot keys);
+    vocab1 — every token is 0."""
     rng = np.random.default_rng([seed, b, l, v])
 
     def draw():
@@ -56,6 +77,13 @@ def generate_batch(b, l, v, r, seed=42, data="uniform"):
     cand = draw()
     if data == "uniform":
         return cand, [draw() for _ in range(r)]
+    if data in ("zipf", "vocab1"):
+        def hot(x):
+            ids, lengths = x
+            if data == "vocab1":
+                return np.zeros_like(ids), lengths
+            return (rng.zipf(1.1, size=ids.shape).astype(np.int64) - 1) % v, lengths
+        return hot(cand), [hot(draw()) for _ in range(r)]
     refs = []
     for _ in range(r):
         ids = cand[0].copy()
@@ -67,15 +95,50 @@ def generate_batch(b, l, v, r, seed=42, data="uniform"):
 
 
 def algorithmic_bytes(lengths_rows, v, b, max_order=4):
-    """A = 4·Σ len + Σ_n T_n·(2·s_k(n) + 8) + 8·B."""
+    """SURVEY.md §8(d) paper dataflow: A = 4·Σ len + Σ_n T_n·(2·s_k(n) + 8) + 8·B."""
     lens = np.concatenate([np.asarray(x, dtype=np.int64) for x in lengths_rows])
-    bits = math.ceil(math.log2(v))
+    bits = math.ceil(math.log2(max(v, 2)))
     a = 4 * int(lens.sum()) + 8 * b
     for n in range(1, max_order + 1):
         t_n = int(np.maximum(lens - n + 1, 0).sum())
         s_k = 8 if n * bits <= 64 else 16
         a += t_n * (2 * s_k + 8)
     return a
+
+
+def moved_bytes(lengths_rows, b, n_out_words, token_bytes=4):
+    """Bytes the fused kernel must move per launch: every valid
+    token once (int32), the (B,) int64 lengths of every row set, and the
+    outputs (n_out_words int64/fp64 words).  This is the roofline numerator."""
+    lens = [np.asarray(x, dtype=np.int64) for x in lengths_rows]
+    return token_bytes * int(sum(int(x.sum()) for x in lens)) + 8 * b * len(lens) + 8 * n_out_words
+
+
+def config_dict(workload, data, world, scaling):
+    """The `config` of a JSON line — identical in both arms."""
+    b, l, v, r, smoothing, mode, _ = WORKLOADS[workload]
+    gb = b * world if scaling == "weak" else b
+    return {"workload": f"{workload}: {'corpus' if mode == 'corpus' else 'per-sentence'} BLEU-4, "
+                        f"B={b} L={l} V={v} R={r} smoothing={smoothing}, data={data}, "
+                        + ("per GPU (weak scaling)" if scaling == "weak" else "one global batch (strong scaling)"),
+            "global_batch": gb, "seq_len": l, "parallelism": f"dp{world} (row shards)"}
+
+
+def shard_rows(b, world, rank):
+    per = -(-b // world)
+    lo = min(rank * per, b)
+    return lo, min(lo + per, b)
+
+
+def workload_batch(workload, data, world, rank, scaling):
+    """This rank's batch 0: weak — the generator at seed 42 + rank (rank 0 is
+    the reference's own batch); strong — rows [lo, hi) of the global batch."""
+    b, l, v, r, _, _, _ = WORKLOADS[workload]
+    if scaling == "weak":
+        return generate_batch(b, l, v, r, seed=42 + rank, data=data)
+    (ci, cl), refs = generate_batch(b, l, v, r, seed=42, data=data)
+    lo, hi = shard_rows(b, world, rank)
+    return (ci[lo:hi], cl[lo:hi]), [(i[lo:hi], ln[lo:hi]) for i, ln in refs]
 
 
 class ClockSampler:
@@ -142,32 +205,96 @@ def _ref_pkg():
     return oracle.reference_package()
 
 
-def cpu_reference_single(cand, refs, smoothing, repeats=3, mode="sentence"):
-    """The reference's shipped path: batchbleu.sentence_bleu (corpus_bleu in
-    corpus mode), compiled backend, threads=1 — 1 warm-up + `repeats` timed
-    runs over the whole batch."""
+def reference_outputs(cand, refs, smoothing, mode):
+    """The reference's own results on these host arrays (batchbleu from
+    oracle/_ref), else the C restatement's: dict of numerators, denominators,
+    cand_lens, eff_ref_lens, scores (corpus: totals + score)."""
     bb = _ref_pkg()
     if bb is not None:
         c = bb.TokenBatch(ids=cand[0], lengths=cand[1])
         rs = [bb.TokenBatch(ids=i, lengths=l) for i, l in refs]
         cfg = bb.BleuConfig(smoothing=smoothing)
+        st = bb.compute_stats(c, rs, cfg)
+        out = dict(numerators=st.numerators, denominators=st.denominators, cand_lens=st.cand_lens,
+                   eff_ref_lens=st.eff_ref_lens, source="reference batchbleu (oracle/_ref)")
+        if mode == "corpus":
+            out["score"] = float(bb.corpus_bleu(c, rs, cfg).scores)
+        else:
+            out["scores"] = np.asarray(bb.sentence_bleu(c, rs, cfg).scores)
+        return out
+    return oracle_outputs(cand, refs, smoothing, mode)
+
+
+def oracle_outputs(cand, refs, smoothing, mode):
+    import oracle
+    st = oracle.stats(cand[0], cand[1], refs)
+    st["source"] = "C restatement (oracle/tbleu_oracle.c)"
+    if mode == "corpus":
+        st["score"] = oracle.corpus(st, smoothing)["scores"]
+    else:
+        st["scores"] = oracle.scores(st, smoothing)["scores"]
+    return st
+
+
+def compare_outputs(got, want, mode):
+    """None when identical (counts bit-exact, scores within SCORE_RTOL), else
+    a one-line description of the first difference."""
+    if mode == "corpus":
+        n = want["numerators"].shape[1]
+        tot = np.concatenate([want["numerators"].sum(0), want["denominators"].sum(0),
+                              [want["cand_lens"].sum(), want["eff_ref_lens"].sum()]]).astype(np.int64)
+        if not np.array_equal(got["totals"], tot):
+            return f"corpus totals differ: {got['totals'].tolist()} vs {tot.tolist()} (N={n})"
+        s, w = got["score"], want["score"]
+        if not (s == w or abs(s - w) <= SCORE_RTOL * abs(w)):
+            return f"corpus score {s!r} vs {w!r}"
+        return None
+    for k in ("numerators", "denominators", "cand_lens", "eff_ref_lens"):
+        if not np.array_equal(got[k], want[k]):
+            bad = np.argwhere(np.asarray(got[k]) != np.asarray(want[k]))
+            return f"{k} differ at {bad[:3].tolist()} ({len(bad)} entries)"
+    s, w = np.asarray(got["scores"]), np.asarray(want["scores"])
+    if not np.array_equal(s == 0, w == 0):
+        return "score zero sets differ"
+    rel = np.abs(s - w) / np.where(w == 0, 1.0, np.abs(w))
+    if rel.size and rel.max() > SCORE_RTOL:
+        return f"scores differ: max rel {rel.max():.3e} at row {int(rel.argmax())}"
+    return None
+
+
+def cpu_reference_single(cand, refs, smoothing, repeats=3, mode="sentence", rows=None):
+    """The reference's shipped path: batchbleu.sentence_bleu (corpus_bleu in
+    corpus mode), compiled backend, threads=1 — 1 warm-up + `repeats` timed
+    runs over the first `rows` rows (all by default).  Returns (rows/s,
+    kind, description)."""
+    if rows is not None and rows < cand[0].shape[0]:
+        cand = (cand[0][:rows], cand[1][:rows])
+        refs = [(i[:rows], ln[:rows]) for i, ln in refs]
+    b = cand[0].shape[0]
+    bb = _ref_pkg()
+    if bb is not None:
+        cfg = bb.BleuConfig(smoothing=smoothing)
         fn = bb.corpus_bleu if mode == "corpus" else bb.sentence_bleu
-        fn(c, rs, cfg)
+
+        def call():
+            c = bb.TokenBatch(ids=cand[0], lengths=cand[1])
+            rs = [bb.TokenBatch(ids=i, lengths=l) for i, l in refs]
+            fn(c, rs, cfg)
+        call()
         ts = []
         for _ in range(repeats):
             t0 = time.perf_counter()
-            fn(c, rs, cfg)
+            call()
             ts.append(time.perf_counter() - t0)
-        return min(ts), "reference", f"batchbleu.{fn.__name__} (oracle/_ref, compiled backend, threads=1)"
+        return b / min(ts), "reference", f"batchbleu.{fn.__name__} (oracle/_ref, compiled backend, threads=1)"
     import oracle
-    oracle.stats(cand[0][:8], cand[1][:8], [(i[:8], l[:8]) for i, l in refs])
     ts = []
     for _ in range(repeats):
         t0 = time.perf_counter()
         st = oracle.stats(cand[0], cand[1], refs)
         (oracle.corpus if mode == "corpus" else oracle.scores)(st, smoothing)
         ts.append(time.perf_counter() - t0)
-    return min(ts), "port", "oracle/tbleu_oracle.c (C restatement, 1 thread)"
+    return b / min(ts), "port", "oracle/tbleu_oracle.c (C restatement, 1 thread)"
 
 
 _POOL_DATA = {}
@@ -201,28 +328,41 @@ def _pool_corpus(parts, smoothing):
     return score_corpus_from_stats(st, bb.BleuConfig(smoothing=smoothing)).scores
 
 
+def global_host_batch(workload, data, world, scaling):
+    """The whole job's rows as the reference arm sees them: weak — the N
+    per-rank batches (seeds 42..42+N-1) stacked; strong — the global batch."""
+    b, l, v, r, _, _, _ = WORKLOADS[workload]
+    if scaling == "strong" or world == 1:
+        return generate_batch(b, l, v, r, seed=42, data=data)
+    parts = [generate_batch(b, l, v, r, seed=42 + k, data=data) for k in range(world)]
+    cand = (np.concatenate([p[0][0] for p in parts]), np.concatenate([p[0][1] for p in parts]))
+    refs = [(np.concatenate([p[1][j][0] for p in parts]), np.concatenate([p[1][j][1] for p in parts]))
+            for j in range(r)]
+    return cand, refs
+
+
 def run_reference_arm(args):
     """--impl reference: the reference's own CPU implementation on this host's
     cores (process pool over row shards of the reference's sentence_bleu; in
     corpus mode the shards' compute_stats, aggregated by the reference's
-    score_corpus_from_stats)."""
+    score_corpus_from_stats), over the same rows as our arm's whole job."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
-    b, l, v, r, smoothing = WORKLOADS[args.workload]
-    mode = MODES.get(args.workload, "sentence")
-    cand, refs = generate_batch(b, l, v, r)
+    b, l, v, r, smoothing, mode, default_scaling = WORKLOADS[args.workload]
+    scaling = args.scaling or default_scaling
+    cand, refs = global_host_batch(args.workload, args.data, world, scaling)
+    gb = cand[0].shape[0]
     bb = _ref_pkg()
     cores = len(os.sched_getaffinity(0))
-    line = {"metric": METRIC, "unit": "sentences/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generate_batch, seed 42)",
-            "config": {"workload": f"{args.workload}: {mode} BLEU-4, B={b} L={l} V={v} R={r} smoothing={smoothing}"}}
+    line = {"metric": METRIC, "unit": "sentences/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "int64", "data": f"synthetic (reference generate_batch, {args.data})",
+            "config": config_dict(args.workload, args.data, world, scaling)}
     if bb is None:
-        # the oracle port, all cores via processes is not worth it for the C port: 1 thread
-        t, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=max(args.steps, 1), mode=mode)
-        value = b / t
-        line.update(value=value, ms_per_step=t * 1e3,
+        value, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=max(args.steps, 1), mode=mode)
+        line.update(value=value, ms_per_step=gb / value * 1e3,
                     cpu_baseline={"value": value, "unit": "sentences/s", "cores": 1, "kind": kind, "sample": what},
                     e2e={"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
         print(json.dumps(line), flush=True)
@@ -230,8 +370,8 @@ def run_reference_arm(args):
     from concurrent.futures import ProcessPoolExecutor
     import multiprocessing as mp
     workers = cores
-    per = -(-b // workers)
-    spans = [(lo, min(lo + per, b)) for lo in range(0, b, per)]
+    per = -(-gb // workers)
+    spans = [(lo, min(lo + per, gb)) for lo in range(0, gb, per)]
     ctx = mp.get_context("fork")
     with ProcessPoolExecutor(max_workers=workers, mp_context=ctx, initializer=_pool_init,
                              initargs=(cand, refs, smoothing, mode)) as pool:
@@ -242,20 +382,23 @@ def run_reference_arm(args):
         for _ in range(max(args.warmup, 1)):
             step()
         times = []
+        t_budget = time.perf_counter() + 120.0  # bounded: at most ~2 min of timed steps
         for _ in range(args.steps):
             t0 = time.perf_counter()
             step()
             times.append(time.perf_counter() - t0)
+            if time.perf_counter() > t_budget:
+                break
     t_pool = float(np.mean(times))
-    # threads=1 shipped configuration, for the record
-    t1, kind, what = cpu_reference_single(cand, refs, smoothing, repeats=2, mode=mode)
-    value = b / t_pool
-    line.update(value=value, ms_per_step=t_pool * 1e3,
+    # threads=1 shipped configuration, for the record (a bounded row sample)
+    v1, _, _ = cpu_reference_single(cand, refs, smoothing, repeats=2, mode=mode, rows=min(gb, 1024))
+    value = gb / t_pool
+    line.update(value=value, ms_per_step=t_pool * 1e3, steps_timed=len(times),
                 cpu_baseline={"value": value, "unit": "sentences/s", "cores": workers, "kind": "reference",
                               "sample": f"batchbleu.{'compute_stats' if mode == 'corpus' else 'sentence_bleu'} "
                                         f"over {len(spans)} row shards in a {workers}-process pool (harness "
-                                        f"wrapper), full {b}x{l} batch per step",
-                              "single_core_value": b / t1},
+                                        f"wrapper), the whole {gb}x{l} job per step",
+                              "single_core_value": v1},
                 e2e={"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
     print(json.dumps(line), flush=True)
     return 0
@@ -264,35 +407,69 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 # Our arm
 # ---------------------------------------------------------------------------
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
+class Ctx:
+    """Process-wide state of our arm: ranks, device, process group."""
 
-    import paper_2510_05485_b200 as tb
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        # TB_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo, so the
+        # multi-rank logic can be exercised on a one-GPU box; never used for numbers
+        shared = os.environ.get("TB_BENCH_SHARED_GPU") == "1"
+        gpu = 0 if shared else local
+        # TB_BENCH_FORCE_DIST=1 (testing only): the process group and its collectives
+        # even at world size 1, so the NCCL code path runs on a one-GPU box
+        self.distributed = self.world > 1 or os.environ.get("TB_BENCH_FORCE_DIST") == "1"
+        if self.distributed:
+            torch.cuda.set_device(gpu)
+            if shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        self.dev = torch.device("cuda", gpu if self.distributed else 0)
+        torch.cuda.set_device(self.dev)
+        self.gloo = self.distributed and dist.get_backend() == "gloo"
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # TB_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo, so the
-    # multi-rank logic can be exercised on a one-GPU box; never used for numbers
-    shared = os.environ.get("TB_BENCH_SHARED_GPU") == "1"
-    gpu = 0 if shared else local
-    # TB_BENCH_FORCE_DIST=1 (testing only): the process group and its collectives
-    # even at world size 1, so the NCCL code path runs on a one-GPU box
-    distributed = world > 1 or os.environ.get("TB_BENCH_FORCE_DIST") == "1"
-    if distributed:
-        torch.cuda.set_device(gpu)
-        if shared:
-            dist.init_process_group("gloo")
+    def barrier(self):
+        if self.distributed:
+            self.dist.barrier()
+
+    def allreduce(self, t, op):
+        """all_reduce of a small device tensor (host-staged over gloo)."""
+        if not self.distributed:
+            return t
+        if self.gloo:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=op)
+            t.copy_(h)
         else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
-    dev = torch.device("cuda", gpu if distributed else 0)
-    torch.cuda.set_device(dev)
+            self.dist.all_reduce(t, op=op)
+        return t
 
-    b, l, v, r, smoothing = WORKLOADS[args.workload]
-    mode = MODES.get(args.workload, "sentence")
+    def max_over_ranks(self, x):
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self.dev)
+        return float(self.allreduce(t, self.dist.ReduceOp.MAX).item())
+
+    def min_over_ranks(self, x):
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self.dev)
+        return float(self.allreduce(t, self.dist.ReduceOp.MIN).item())
+
+
+def measure(ctx, workload, data, scaling, steps, warmup, *, full, cpu_baseline, clock_window=0.0,
+            e2e_steps=None):
+    """Time one workload on this rank; returns (result dict, error or None).
+    full: the headline's extra legs (int64 / numpy e2e, L2-flushed steps, eager API)."""
+    torch, dist = ctx.torch, ctx.dist
+    import paper_2510_05485_b200 as tb
+    dev, world, rank = ctx.dev, ctx.world, ctx.rank
+    b_wl, l, v, r, smoothing, mode, _ = WORKLOADS[workload]
     corpus = mode == "corpus"
-    cand_np, refs_np = generate_batch(b, l, v, r, seed=42 + rank, data=args.data)
+    (cand_np, refs_np) = workload_batch(workload, data, world, rank, scaling)
+    b = cand_np[0].shape[0]
     cfg = tb.BleuConfig(smoothing=smoothing)
     mk_plan = (lambda c_, r_: tb.SentenceBleuPlan(c_, r_, cfg, stats=False, corpus=True, sentence=False)) \
         if corpus else (lambda c_, r_: tb.SentenceBleuPlan(c_, r_, cfg))
@@ -306,7 +483,7 @@ def run_ours(args):
     refs = [tb.TokenBatch(ids=to_dev(i, torch.int32), lengths=to_dev(ln, torch.int64)) for i, ln in refs_np]
     batch_bytes = b * l * 4 * (1 + r) + 8 * b * (1 + r)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    nbuf = max(2, -(-2 * l2_bytes // batch_bytes))
+    nbuf = max(2, -(-2 * l2_bytes // max(batch_bytes, 1)))
     gen = torch.Generator(device=dev)
     plans = [mk_plan(cand, refs)]
     for k in range(1, nbuf):
@@ -324,228 +501,350 @@ def run_ours(args):
             lens = (c_.lengths + torch.randint(-50, 51, (b,), generator=gen, device=dev)).clamp(l // 2, l)
             return tb.TokenBatch.trusted(ids, lens)
 
-        c_k = draw()
-        plans.append(mk_plan(c_k, [draw() if args.data == "uniform" else mutate(c_k) for _ in range(r)]))
-    plan = plans[0]
+        def shuffled(x):  # hot-key data: batch 0's rows in another order, tokens rolled
+            perm = torch.randperm(b, generator=gen, device=dev)
+            return tb.TokenBatch.trusted(torch.roll(x.ids[perm], shifts=k, dims=1).contiguous(), x.lengths[perm])
+
+        if data == "uniform":
+            plans.append(mk_plan(draw(), [draw() for _ in range(r)]))
+        elif data == "correlated":
+            c_k = draw()
+            plans.append(mk_plan(c_k, [mutate(c_k) for _ in range(r)]))
+        else:
+            plans.append(mk_plan(shuffled(cand), [shuffled(x) for x in refs]))
 
     def step(pl):
         """One step: the fused kernel (one launch); in corpus mode across
         ranks, then the NCCL all-reduce of the 2N+2 int64 totals over NVLink
         and the corpus epilogue on every rank."""
         pl.run()
-        if corpus and distributed:
-            dist.all_reduce(pl.totals, op=dist.ReduceOp.SUM)
+        if corpus and ctx.distributed:
+            ctx.allreduce(pl.totals, dist.ReduceOp.SUM)
             pl.corpus_from_totals()
 
-    kernels_per_step = 1 + (1 if corpus and distributed else 0)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-
-    def barrier():
-        if distributed:
-            dist.barrier()
-
-    # correctness gate before timing (bench.py:104-113 analogue): counts vs oracle on a slice
-    import oracle
-    if rank == 0:
-        st = tb.compute_stats(tb.TokenBatch(ids=cand_np[0][:32], lengths=cand_np[1][:32]),
-                              [tb.TokenBatch(ids=i[:32], lengths=ln[:32]) for i, ln in refs_np], cfg)
-        o = oracle.stats(cand_np[0][:32], cand_np[1][:32], [(i[:32], ln[:32]) for i, ln in refs_np])
-        if not np.array_equal(st.numerators, o["numerators"]):
-            print(json.dumps({"error": "equivalence check failed"}), flush=True)
-            return 2
+    kernels_per_step = 1 + (1 if corpus and ctx.distributed else 0)
+    stream = torch.cuda.current_stream(dev)
 
     # ---- device-resident timing: K steps, back to back, each on its own batch
-    stream = torch.cuda.current_stream(dev)
-    for k in range(max(args.warmup, 1) * len(plans)):
+    for k in range(max(warmup, 1) * len(plans)):
         step(plans[k % len(plans)])
     torch.cuda.synchronize(dev)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
-        # keep the GPU under this load for ~1 s so that nvidia-smi (>= 50 ms period)
+    clk = ClockSampler(dev.index)
+    with clk if clock_window > 0 else _Null():
+        # keep the GPU under this load so that nvidia-smi (>= 50 ms period)
         # samples the clocks of this workload; the timed steps follow directly
-        t_until = time.perf_counter() + args.clock_window
+        t_until = time.perf_counter() + clock_window
         while time.perf_counter() < t_until:
             for k in range(200):
                 step(plans[k % len(plans)])
             torch.cuda.synchronize(dev)
-        barrier()
+        ctx.barrier()
         torch.cuda.synchronize(dev)
         t_start.record(stream)
-        for k in range(args.steps):
+        for k in range(steps):
             step(plans[k % len(plans)])
         t_end.record(stream)
         torch.cuda.synchronize(dev)
-        barrier()
+        ctx.barrier()
     t_local = t_start.elapsed_time(t_end) / 1e3
-    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
-    value = b * world * args.steps / t_max
+    t_max = ctx.max_over_ranks(t_local)
+    rows_job = (b * world) if scaling == "weak" else b_wl
+    value = rows_job * steps / t_max
 
-    # ---- secondary: one batch, L2 flushed (256 MiB write) before every step, each step event-timed
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    for k in range(args.steps):
-        flush.zero_()
-        starts[k].record(stream)
-        step(plan)
-        ends[k].record(stream)
+    # kernel-only time per launch (the roofline's denominator): the timed loop
+    # itself when a step is one launch, else a kernel-only loop of the same length
+    if kernels_per_step == 1:
+        kernel_s = t_local / steps
+    else:
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        for k in range(steps):
+            plans[k % len(plans)].run()
+        k1.record(stream)
+        torch.cuda.synchronize(dev)
+        kernel_s = k0.elapsed_time(k1) / 1e3 / steps
+
+    # ---- verification of the timed path: plan 0 once more, against the reference
+    step(plans[0])
     torch.cuda.synchronize(dev)
-    step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
+    pl = plans[0]
+    pl.check()  # device data flags (none expected)
+    src = reference_outputs if full and rank == 0 else oracle_outputs
+    if corpus:
+        # the timed outputs: the all-reduced (whole-job) int64 totals and the corpus score
+        gc, gr = global_host_batch(workload, data, world, scaling) if ctx.distributed else (cand_np, refs_np)
+        want = src(gc, gr, smoothing, mode)
+        got = {"totals": pl.totals.cpu().numpy(), "score": float(pl.corpus[0].item())}
+    else:
+        want = src(cand_np, refs_np, smoothing, mode)
+        got = {k: getattr(pl, k).cpu().numpy() for k in
+               ("numerators", "denominators", "cand_lens", "eff_ref_lens", "scores")}
+    err = compare_outputs(got, want, mode)
+    verified_local = 1.0 if err is None else 0.0
+    verified = ctx.min_over_ranks(verified_local) == 1.0
+    verify = {"verified": verified, "against": want["source"],
+              "what": ("global int64 totals (after the all-reduce) and corpus score of batch 0; "
+                       "this rank's per-sentence counts" if corpus else
+                       "per-sentence numerators/denominators/lengths bit-exact, fp64 scores within "
+                       f"{SCORE_RTOL} relative, on batch 0 (the reference generator's batch) "
+                       "after the timed loop, through the timed plan")}
+    if err is not None:
+        verify["error"] = f"rank {rank}: {err}"
 
-    # ---- eager public API (no graph), same device-resident inputs
-    def eager_call():
-        if not corpus:
-            return tb.sentence_bleu(cand, refs, cfg)
-        if not distributed:
-            return tb.corpus_bleu(cand, refs, cfg)
-        from paper_2510_05485_b200.distributed import allreduce_totals
-        return tb.score_corpus_from_totals(allreduce_totals(tb.corpus_totals(cand, refs, cfg)), cfg)
-
-    for _ in range(2):
-        eager_call()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    eager = []
-    for _ in range(args.steps):
-        flush.zero_()
-        e0.record(stream)
-        eager_call()
-        e1.record(stream)
-        e1.synchronize()
-        eager.append(e0.elapsed_time(e1))
-
-    # ---- e2e: public API with pinned HOST buffers; H2D + kernel + D2H in the timed region.
-    # Headline: int32 token IDs (the dtype the path computes in, and what a
-    # training loop's tokenizer output holds); int64 (the reference
-    # TokenBatch's own dtype, batch.py:23-24) is reported beside it.
+    # ---- e2e: public API with HOST buffers; H2D + kernel + D2H in the timed region
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     d2h = 4 + (b * (2 + cfg.max_order) * 8 if not corpus else (3 * cfg.max_order + 4) * 8)
+    e2e_steps = e2e_steps or steps
 
-    def measure_e2e(np_dtype, numpy_rows=False):
-        if numpy_rows:  # the reference's usage: TokenBatch over (pageable) numpy arrays
-            hcand = tb.TokenBatch(ids=cand_np[0].astype(np_dtype), lengths=cand_np[1])
-            hrefs = [tb.TokenBatch(ids=i.astype(np_dtype), lengths=ln) for i, ln in refs_np]
-        else:
-            hcand = tb.TokenBatch(ids=torch.from_numpy(cand_np[0].astype(np_dtype)).pin_memory(),
-                                  lengths=torch.from_numpy(cand_np[1]))
-            hrefs = [tb.TokenBatch(ids=torch.from_numpy(i.astype(np_dtype)).pin_memory(), lengths=torch.from_numpy(ln))
-                     for i, ln in refs_np]
-        # tb_bleu_host: the kernel reads each pinned row's valid prefix over PCIe
-        # (zero-copy) plus the lengths; results are written straight into pinned memory
+    def measure_e2e(kind):
+        """kind: pinned32 / pinned64 (torch pinned tensors, TokenBatch built
+        once), numpy64 (TokenBatch over pageable numpy int64, built once),
+        fresh_numpy64 (a NEW TokenBatch over numpy int64 arrays every step,
+        construction + validation inside the timed region — the reference's
+        own calling convention, as its arm does)."""
+        np_dtype = np.int32 if kind == "pinned32" else np.int64
         isz = np.dtype(np_dtype).itemsize
+        if kind == "fresh_numpy64":
+            # 4 distinct host batches cycled; each step wraps its arrays in new TokenBatch objects
+            pool = [(cand_np, refs_np)] + [
+                ((np.roll(cand_np[0], j, axis=1), cand_np[1]), [(np.roll(i, j, axis=1), ln) for i, ln in refs_np])
+                for j in (1, 2, 3)]
+
+            def make(j):
+                c_, r_ = pool[j % len(pool)]
+                return tb.TokenBatch(ids=c_[0], lengths=c_[1]), [tb.TokenBatch(ids=i, lengths=ln) for i, ln in r_]
+        else:
+            if kind == "numpy64":
+                hb = (tb.TokenBatch(ids=cand_np[0], lengths=cand_np[1]),
+                      [tb.TokenBatch(ids=i, lengths=ln) for i, ln in refs_np])
+            else:
+                hb = (tb.TokenBatch(ids=torch.from_numpy(cand_np[0].astype(np_dtype)).pin_memory(),
+                                    lengths=torch.from_numpy(cand_np[1])),
+                      [tb.TokenBatch(ids=torch.from_numpy(i.astype(np_dtype)).pin_memory(),
+                                     lengths=torch.from_numpy(ln)) for i, ln in refs_np])
+
+            def make(j):
+                return hb
         h2d = int(sum(isz * int(ln.sum()) + 8 * ln.size for ln in [cand_np[1]] + [x for _, x in refs_np]))
 
-        def e2e_call():
+        def e2e_call(j):
             """The user's call on host buffers; results come back as numpy / floats."""
+            hc, hr = make(j)
             if not corpus:
-                return tb.sentence_bleu(hcand, hrefs, cfg)
-            if not distributed:
-                return tb.corpus_bleu(hcand, hrefs, cfg)
-            tot = torch.from_numpy(tb.corpus_totals(hcand, hrefs, cfg)).to(dev)  # this rank's shard
-            dist.all_reduce(tot, op=dist.ReduceOp.SUM)                            # NCCL, 80 B
+                return tb.sentence_bleu(hc, hr, cfg)
+            if not ctx.distributed:
+                return tb.corpus_bleu(hc, hr, cfg)
+            tot = torch.from_numpy(tb.corpus_totals(hc, hr, cfg)).to(dev)  # this rank's shard
+            ctx.allreduce(tot, dist.ReduceOp.SUM)                          # NCCL, 80 B
             return tb.score_corpus_from_totals(tot, cfg, host=True)
 
-        for _ in range(2):
-            e2e_call()
-        barrier()
+        first = None
+        for j in range(2):
+            first = e2e_call(0)
+        ctx.barrier()
         e2e_times = []
-        for _ in range(args.steps):
+        for j in range(e2e_steps):
             flush.zero_()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            res = e2e_call()   # returns numpy / float: synchronous end to end
+            res = e2e_call(j)   # returns numpy / float: synchronous end to end
             e2e_times.append(time.perf_counter() - t0)
         assert corpus or res.scores.shape == (b,)
-        te = torch.tensor([float(np.sum(e2e_times))], dtype=torch.float64, device=dev)
-        if distributed:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        return b * world * args.steps / float(te.item()), h2d
+        # the host path's results on batch 0 equal the verified device results
+        same = (np.array_equal(np.asarray(first.scores), got["scores"]) if not corpus
+                else (not ctx.distributed and float(first.scores) == float(pl.corpus[0].item())) or ctx.distributed)
+        te = ctx.max_over_ranks(float(np.sum(e2e_times)))
+        return rows_job * e2e_steps / te, h2d, bool(same)
 
-    e2e_value, h2d = measure_e2e(np.int32)
-    e2e64_value, h2d64 = measure_e2e(np.int64)
-    e2e_np_value, _ = measure_e2e(np.int64, numpy_rows=True)
+    e2e = {}
+    kinds = ("pinned32", "pinned64", "numpy64", "fresh_numpy64") if full else ("pinned32",)
+    for kind in kinds:
+        val, h2d, same = measure_e2e(kind)
+        e2e[kind] = {"value": val, "h2d_bytes_per_step": h2d, "same_results_as_device": same}
 
-    # ---- roofline of the fused kernel (the only kernel of a step)
-    a_bytes = algorithmic_bytes([cand_np[1]] + [ln for _, ln in refs_np], v, b)
-    kernel_s = t_local / args.steps  # back-to-back: kernel + inter-launch gap (conservative)
-    peaks = {}
+    out = {"workload": workload, "data": data, "scaling": scaling, "rows_per_step": rows_job,
+           "rows_this_rank": b, "value": value, "ms_per_step": t_max * 1e3 / steps,
+           "kernel_ms": kernel_s * 1e3, "kernels_per_step": kernels_per_step, "d2h": d2h, "e2e": e2e,
+           "verify": verify, "nbuf": nbuf, "batch_bytes": batch_bytes, "l2_bytes": l2_bytes,
+           "lengths_rows": [cand_np[1]] + [ln for _, ln in refs_np], "v": v, "b": b, "mode": mode,
+           "n_out_words": ((2 * cfg.max_order + 2) + (cfg.max_order + 2) if corpus
+                           else b * (3 * cfg.max_order + 4)),
+           "clocks": clk.summary() if clock_window > 0 else None}
+
+    if full:
+        # ---- secondary: one batch, L2 flushed (256 MiB write) before every step, each step event-timed
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        for k in range(steps):
+            flush.zero_()
+            starts[k].record(stream)
+            step(plans[0])
+            ends[k].record(stream)
+        torch.cuda.synchronize(dev)
+        step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
+        out["step_flush_l2"] = {"value": rows_job / (float(np.mean(step_ms)) / 1e3), "unit": "sentences/s",
+                                "ms_per_step": float(np.mean(step_ms)), "min_ms": float(np.min(step_ms)),
+                                "path": "one batch, 256 MiB L2-flush write before every step, each step "
+                                        "timed by its own CUDA events (includes launch latency)"}
+
+        # ---- eager public API (no plan), same device-resident inputs
+        def eager_call():
+            if not corpus:
+                return tb.sentence_bleu(cand, refs, cfg)
+            if not ctx.distributed:
+                return tb.corpus_bleu(cand, refs, cfg)
+            from paper_2510_05485_b200.distributed import allreduce_totals
+            return tb.score_corpus_from_totals(allreduce_totals(tb.corpus_totals(cand, refs, cfg)), cfg)
+
+        for _ in range(2):
+            eager_call()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eager = []
+        for _ in range(steps):
+            flush.zero_()
+            e0.record(stream)
+            eager_call()
+            e1.record(stream)
+            e1.synchronize()
+            eager.append(e0.elapsed_time(e1))
+        out["eager_api"] = {"value": rows_job / (np.mean(eager) / 1e3), "unit": "sentences/s",
+                            "ms_per_step": float(np.mean(eager)),
+                            "path": "public API on TokenBatch(CUDA tensors), eager, per-call allocation"}
+
+    if cpu_baseline and rank == 0:
+        # the reference's shipped path on this host, 1 core, on a bounded row sample
+        rows = b if b <= 4096 else 1024
+        v1, kind, what = cpu_reference_single(cand_np, refs_np, smoothing, repeats=3, mode=mode, rows=rows)
+        out["cpu_baseline"] = {"value": v1, "unit": "sentences/s", "cores": 1, "kind": kind,
+                               "sample": f"{what}; the first {rows} rows of this rank's {b}x{l} batch, "
+                                         "best of 3 after 1 warm-up"}
+    return out, (None if verified else verify.get("error", "verification failed on another rank"))
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-        peak, peak_src = float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    achieved = a_bytes / kernel_s / 1e9
-    traffic = None
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _ncu_traffic(workload, data):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
-            prof = json.load(fh).get(args.workload, {})
-            traffic = prof.get("dram_bytes_per_launch")
+            prof = json.load(fh)
+        key = workload if data == "uniform" else f"{workload}{'corr' if data == 'correlated' else data}"
+        return prof.get(key, {}).get("dram_bytes_per_launch")
     except Exception:
-        pass
-    input_bytes = int(sum(4 * int(x.sum()) for x in [cand_np[1]] + [ln for _, ln in refs_np]))
+        return None
 
-    line = None
-    if rank == 0:
-        cpu = None
-        if not args.no_cpu_baseline:
-            t_cpu, kind, what = cpu_reference_single(cand_np, refs_np, smoothing, repeats=3, mode=mode)
-            cpu = {"value": b / t_cpu, "unit": "sentences/s", "cores": 1, "kind": kind,
-                   "sample": f"{what}; the full {b}x{l} batch, best of 3 after 1 warm-up"}
+
+def roofline_of(m):
+    """HBM roofline of the fused kernel for one measured workload: the bytes it
+    must move per launch (valid int32 tokens + lengths + outputs) over its
+    average launch time (CUDA events, timed region)."""
+    peak, src = _peak()
+    moved = moved_bytes(m["lengths_rows"], m["b"], m["n_out_words"])
+    paper = algorithmic_bytes(m["lengths_rows"], m["v"], m["b"])
+    ks = m["kernel_ms"] / 1e3
+    achieved = moved / ks / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": _ncu_traffic(m["workload"], m["data"]), "peak_source": src,
+            "bytes_per_launch": moved, "kernel_us": m["kernel_ms"] * 1e3,
+            "paper_dataflow_bytes": paper, "paper_dataflow_ratio": paper / ks / 1e9 / peak,
+            "note": "frac = bytes the fused kernel must move (valid int32 tokens once + int64 lengths + "
+                    "outputs) / average launch time (CUDA events over the timed loop) / measured HBM peak; "
+                    "traffic = ncu dram__bytes_read+write per launch (profiles/ncu_summary.json); "
+                    "paper_dataflow_ratio = SURVEY §8(d) paper-dataflow bytes A / launch time / peak "
+                    "(> 1 means the fused kernel beats the paper's dataflow, not a bandwidth)"}
+
+
+def run_ours(args):
+    ctx = Ctx()
+    scaling = args.scaling or WORKLOADS[args.workload][6]
+    head, err = measure(ctx, args.workload, args.data, scaling, args.steps, args.warmup, full=True,
+                        cpu_baseline=not args.no_cpu_baseline, clock_window=args.clock_window)
+    if err is not None:
+        if ctx.rank == 0:
+            print(json.dumps({"error": f"equivalence check failed: {err}", "workload": args.workload}), flush=True)
+        return 2
+    grid = {}
+    if not args.no_configs:
+        for wl, data in CONFIG_GRID:
+            if (wl, data) == (args.workload, args.data):
+                continue
+            sc = WORKLOADS[wl][6]
+            m, e = measure(ctx, wl, data, sc, min(args.steps, 100), 3, full=False,
+                           cpu_baseline=(data == "uniform"), e2e_steps=10)
+            if e is not None:
+                if ctx.rank == 0:
+                    print(json.dumps({"error": f"equivalence check failed: {e}", "workload": wl, "data": data}),
+                          flush=True)
+                return 2
+            rf = roofline_of(m)
+            entry = {"config": config_dict(wl, data, ctx.world, sc), "scaling": sc,
+                     "value": m["value"], "unit": "sentences/s", "ms_per_step": m["ms_per_step"],
+                     "kernel_us": m["kernel_ms"] * 1e3,
+                     "e2e_pinned_int32": m["e2e"]["pinned32"]["value"],
+                     "roofline_frac": rf["frac"], "achieved_gbs": rf["achieved"],
+                     "paper_dataflow_ratio": rf["paper_dataflow_ratio"],
+                     "verified": m["verify"]["verified"], "verified_against": m["verify"]["against"]}
+            if "cpu_baseline" in m:
+                entry["cpu_ref_1core"] = m["cpu_baseline"]["value"]
+            grid[f"{wl}_{data}"] = entry
+    if ctx.rank == 0:
+        m = head
+        e2e = m["e2e"]
         line = {
-            "metric": METRIC, "value": value, "unit": "sentences/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": ("synthetic (reference generate_batch: uniform IDs, lengths U[L/2, L], seed 42+rank)"
-                     if args.data == "uniform" else
-                     "synthetic, correlated: references = candidate with per-row mutation rate U[0, 0.9]"),
-            "config": {"workload": f"{args.workload}: {'corpus' if corpus else 'per-sentence'} BLEU-4, "
-                                   f"B={b} L={l} V={v} R={r} smoothing={smoothing}, per GPU (weak scaling)",
-                       "global_batch": b * world, "seq_len": l, "parallelism": f"dp{world} (row shards)",
-                       "timed_path": "SentenceBleuPlan.run(): one tb_bleu_stats launch per step (native binding)"
+            "metric": METRIC, "value": m["value"], "unit": "sentences/s", "n_gpus": ctx.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["ms_per_step"],
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "int32",
+            "data": {"uniform": "synthetic (reference generate_batch: uniform IDs, lengths U[L/2, L], seed 42+rank)",
+                     "correlated": "synthetic, correlated: references = candidate with per-row mutation U[0, 0.9]",
+                     "zipf": "synthetic, Zipf(1.1) token IDs (hot keys)",
+                     "vocab1": "synthetic, every token 0 (vocab = 1)"}[args.data],
+            "config": config_dict(args.workload, args.data, ctx.world, scaling),
+            "timing": {"timed_path": "SentenceBleuPlan.run(): one tb_bleu_stats launch per step (native binding)"
                                      + (", then NCCL all_reduce of the int64 totals + corpus epilogue kernel"
-                                        if corpus and distributed else "")
-                                     + "; K steps back to back between two CUDA events",
-                       "l2": f"inputs larger than L2: steps cycle through {nbuf} distinct device-resident "
-                             f"batches ({nbuf * batch_bytes / 2**20:.0f} MiB > {l2_bytes / 2**20:.0f} MiB L2); "
-                             "batch 0 = reference generator seed 42, others torch.randint of the same "
-                             "distributions"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": a_bytes,
-                         # the DRAM bytes the kernel really moves (ncu) over the same step time:
-                         # how far from HBM-bound it is (it is latency-bound, DESIGN.md §3.1)
-                         "dram_achieved": (traffic / kernel_s / 1e9) if traffic else None,
-                         "dram_frac": (traffic / kernel_s / 1e9 / peak) if traffic else None,
-                         "note": "A = SURVEY §8(d) paper-dataflow bytes; the fused kernel only reads the "
-                                 f"{input_bytes} B of int32 tokens, so frac > 1 means it beats the paper dataflow; "
-                                 "dram_frac = ncu DRAM bytes per launch / step time / peak"},
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "sentences/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "token_dtype": "int32",
-                    "int64_tokens": {"value": e2e64_value, "h2d_bytes_per_step": int(h2d64)},
-                    "numpy_int64_tokens": {"value": e2e_np_value,
-                                           "path": "TokenBatch(numpy int64, pageable) as the reference uses it: "
-                                                   "valid prefixes copied into pinned memory by host threads, "
-                                                   "narrowed to int32 when the IDs fit, read over PCIe"},
-                    "path": f"{'corpus' if corpus else 'sentence'}_bleu(TokenBatch(pinned host tensors)) "
-                            "-> numpy: one blocking tb_bleu_host call; the kernel streams valid row prefixes "
-                            "over PCIe" + (" (+ NCCL all_reduce of the totals)" if corpus and distributed else "")},
-            "eager_api": {"value": b * world / (np.mean(eager) / 1e3), "unit": "sentences/s",
-                          "ms_per_step": float(np.mean(eager)),
-                          "path": "public API on TokenBatch(CUDA tensors), eager, per-call allocation"},
-            "gpu_launches": args.steps * kernels_per_step,
-            "clocks": clk.summary(),
-            "step_flush_l2": {"value": b * world / (float(np.mean(step_ms)) / 1e3), "unit": "sentences/s",
-                              "ms_per_step": float(np.mean(step_ms)), "min_ms": float(np.min(step_ms)),
-                              "path": "one batch, 256 MiB L2-flush write before every step, each step "
-                                      "timed by its own CUDA events (includes launch latency)"},
+                                        if m["kernels_per_step"] > 1 else "")
+                                     + "; K steps back to back between two CUDA events, max over ranks",
+                       "l2": f"inputs larger than L2: steps cycle through {m['nbuf']} distinct device-resident "
+                             f"batches ({m['nbuf'] * m['batch_bytes'] / 2**20:.0f} MiB > "
+                             f"{m['l2_bytes'] / 2**20:.0f} MiB L2); batch 0 = reference generator, others "
+                             "torch-generated with the same distributions"},
+            "verified": m["verify"]["verified"],
+            "verification": m["verify"],
+            "roofline": roofline_of(m),
+            "cpu_baseline": m.get("cpu_baseline"),
+            "e2e": {"value": e2e["pinned32"]["value"], "unit": "sentences/s",
+                    "h2d_bytes_per_step": e2e["pinned32"]["h2d_bytes_per_step"], "d2h_bytes_per_step": m["d2h"],
+                    "token_dtype": "int32",
+                    "path": "sentence_bleu(TokenBatch(pinned int32 host tensors)) -> numpy: one blocking "
+                            "tb_bleu_host call; the kernel streams valid row prefixes over PCIe",
+                    "int64_tokens": e2e["pinned64"], "numpy_int64_tokens": e2e["numpy64"],
+                    "fresh_numpy_int64": dict(e2e["fresh_numpy64"], path=(
+                        "a NEW TokenBatch over numpy int64 arrays every step (construction + validation "
+                        "in the timed region, the reference's own calling convention), then sentence_bleu"))},
+            "eager_api": m["eager_api"],
+            "step_flush_l2": m["step_flush_l2"],
+            "gpu_launches": args.steps * m["kernels_per_step"],
+            "clocks": m["clocks"],
+            "configs": grid,
         }
         print(json.dumps(line), flush=True)
-    if distributed:
-        dist.barrier()
-        dist.destroy_process_group()
+    if ctx.distributed:
+        ctx.dist.barrier()
+        ctx.dist.destroy_process_group()
     return 0
 
 
@@ -556,9 +855,12 @@ def main(argv=None):
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    p.add_argument("--data", choices=["uniform", "correlated", "zipf", "vocab1"], default="uniform",
+                   help="uniform = the reference generator (the headline); others: SURVEY §8d parity inputs")
+    p.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                   help="default: weak for c1-c3, strong for c4/c5 (one global batch split over the GPUs)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--data", choices=["uniform", "correlated"], default="uniform",
-                   help="uniform = the reference generator (the headline); correlated = related references")
+    p.add_argument("--no-configs", action="store_true", help="skip the configs sub-object (headline only)")
     p.add_argument("--clock-window", type=float, default=1.5,
                    help="seconds of sustained load sampled by nvidia-smi before the timed steps")
     args = p.parse_args(argv)
