@@ -6,9 +6,9 @@
 // Sources of libtensorbleu_b200.so:
 //   tb_common.cuh        this file
 //   tb_launch.cuh        shape planning types + the launch helper
-//   tb_kernel_pair.cu    bleu_pair_kernel (R = 1, round-1 design; fallback)
-//   tb_kernel_sparse.cu  bleu_sparse_kernel (R = 1, warp per group + CTA dense path)
-//   tb_kernel_multi.cu   bleu_multi_kernel (2 <= R <= 8)
+//   tb_kernel_sparse.cu  bleu_sparse_kernel (R <= 8: warp per group; dense groups listed)
+//   tb_kernel_pair.cu    bleu_pair_kernel (R = 1, CTA per group; the listed dense groups)
+//   tb_kernel_multi.cu   bleu_multi_kernel (2 <= R <= 8, CTA per group; the listed dense groups)
 //   tb_kernel_group.cu   bleu_group_kernel (R > 8) and bleu_stats_kernel (global memory)
 //   tb_runtime.cu        planning, launches, host-buffer path, C ABI
 //   plugin.cu            the _backend operator surface
@@ -42,6 +42,8 @@ namespace tbk {
 constexpr int kThreads = 256;
 constexpr int kPairCtasPerSm = 4;  // single-reference kernel: 4 CTAs of kThreads per SM
 constexpr int kMultiMaxRefs = 8;  // references handled by the multi-reference kernel
+constexpr int kSparseMaxRefs = 8;  // references handled by the warp-per-group kernel
+constexpr int kSparseMaxWidth = 4096;  // row widths handled by the warp-per-group kernel
 constexpr int kSmallSet = 128;    // positions matched without a table (<= kThreads)
 constexpr int kMultiThreads = 512;  // multi-reference kernel: 16 warps, 2 CTAs per SM
 constexpr int kAccCopies = 32;         // replicated corpus accumulators (spread L2 atomics)
@@ -111,6 +113,17 @@ struct StatsParams {
   // PCIe); report flags through the completion protocol with a plain store
   int prefix_only;
   int err_store;
+  // warp-group kernel: per-group shared-memory bytes, byte offsets, and the
+  // element offsets of the staged rows (candidate, then reference r)
+  int sp_off_fc, sp_off_fs, sp_off_tok, sp_off_ps, sp_off_aux, sp_off_rows;
+  int sp_row_off[TB_MAX_REFS + 1];
+  int sp_buf_elems;          // elements per row buffer
+  int sp_nbuf;               // row buffers (1 or 2)
+  unsigned int sp_tma_mask;  // bit s: row set s is bulk-copied (16-byte base and pitch)
+  // dense groups listed by the warp-per-group kernel for the CTA-per-group kernel
+  // (list mode when glist != nullptr: that kernel scores glist[0, *gcount))
+  int* glist;
+  unsigned int* gcount;
 };
 
 struct EpiParams {
@@ -181,6 +194,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void griddep_wait_and_release() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// TB_DEBUG_NO_PDL=1: launch the stats kernels without programmatic stream
+// serialization (A/B measurements of the launch overlap)
+// TB_DEBUG_PDL_MODE (A/B only): 1 = list-mode launches keep PDL, 3 = the filter kernel takes it
+inline int pdl_mode() {
+  static const int v = [] {
+    const char* e = getenv("TB_DEBUG_PDL_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+inline bool no_pdl() {
+  static const bool v = [] {
+    const char* e = getenv("TB_DEBUG_NO_PDL");
+    return e && e[0] == '1';
+  }();
+  return v;
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -455,47 +486,82 @@ __device__ void warp_epilogue(int64_t num, int64_t den, int64_t c, int64_t r, in
 // totals) reach the last CTA to finish, which writes *err, runs the corpus
 // epilogue and leaves the workspace zeroed for the next launch.
 // --------------------------------------------------------------------------
-__device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int& s_flags, int& s_last) {
+// The last CTA of a launch: the replicated accumulators summed (one parallel
+// read of all copies) into the totals + the corpus epilogue, the flags moved
+// to *err, and the workspace left zeroed for the next launch.  All threads of
+// the CTA call it; s_tot has >= 2N+2 words.
+__device__ void finalize_launch(const StatsParams& p, unsigned long long* s_tot) {
+  const int tid = threadIdx.x;
+  const int N = p.max_order;
+  const int nt = 2 * N + 2;
+  const bool corpus = p.totals != nullptr || p.corpus != nullptr;
+  if (corpus) {
+    for (int j = tid; j < nt; j += blockDim.x) s_tot[j] = 0;
+    __syncthreads();
+    for (int i = tid; i < kAccCopies * nt; i += blockDim.x) {
+      const unsigned long long v = atomicExch(&p.acc[i], 0ull);
+      if (v) atomicAdd(&s_tot[i % nt], v);
+    }
+    __syncthreads();
+    for (int j = tid; j < nt; j += blockDim.x)
+      if (p.totals) p.totals[j] = static_cast<int64_t>(s_tot[j]);
+  }
+  if (tid == 0) {
+    const int f = atomicExch(p.ws_flag, 0);
+    if (corpus)
+      *p.err = f;  // corpus launches write the flag word
+    else if (f && p.err_store)
+      *p.err |= f;  // host mapped memory: plain stores only (the warp-group kernel may have set bits)
+    else if (f)
+      atomicOr(p.err, f);
+    *p.done = 0;
+    if (p.gcount) *p.gcount = 0;
+  }
+  if (p.corpus && tid < 32) {
+    const int lane = tid;
+    warp_epilogue(lane < N ? static_cast<int64_t>(s_tot[lane]) : 0,
+                  lane < N ? static_cast<int64_t>(s_tot[N + lane]) : 0, static_cast<int64_t>(s_tot[2 * N]),
+                  static_cast<int64_t>(s_tot[2 * N + 1]), N, p.smoothing, p.eps, p.k,
+                  lane < N ? p.weights[lane] : 0.0, p.corpus + 2, p.corpus + 1, p.corpus);
+  }
+}
+
+// Arrival of one CTA at the completion counter (release its updates, acquire
+// everyone else's); true for the last of `participants`.
+__device__ __forceinline__ bool arrive_last(const StatsParams& p, unsigned int participants) {
+  unsigned int prev;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.done) : "memory");
+  return prev == participants - 1;
+}
+
+// End of a CTA of the CTA-per-group kernels.  nb (list mode): the number of
+// listed groups; only the CTAs that got one take part (none when nothing was
+// listed: the warp-group kernel has finished the launch).
+__device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int& s_flags, int& s_last,
+                           int64_t nb = -1) {
   const int tid = threadIdx.x;
   const int N = p.max_order;
   const bool corpus = p.totals != nullptr || p.corpus != nullptr;
-  if (!corpus && !p.err_store) {  // no cross-CTA work: report flags directly (the caller zeroed *err)
+  const bool listed = p.glist != nullptr;
+  if (!corpus && !p.err_store && !listed) {  // no cross-CTA work: report flags directly (the caller zeroed *err)
     __syncthreads();
     if (tid == 0 && s_flags) atomicOr(p.err, s_flags);
     return;
+  }
+  unsigned int participants = gridDim.x;
+  if (listed) {
+    if (nb < 1) return;
+    participants = static_cast<unsigned int>(nb < gridDim.x ? nb : gridDim.x);
+    if (blockIdx.x >= participants) return;  // no group, no flags, no totals
   }
   const int nt = 2 * N + 2;
   __syncthreads();  // s_tot of the last group (warp 0's epilogue) before other threads read it
   if (corpus && tid < nt && s_tot[tid]) atomicAdd(&p.acc[(blockIdx.x % kAccCopies) * nt + tid], s_tot[tid]);
   if (tid == 0 && s_flags) atomicOr(p.ws_flag, s_flags);
   __syncthreads();
-  if (tid == 0) {
-    // release this CTA's accumulator/flag updates, acquire everyone else's
-    unsigned int prev;
-    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.done) : "memory");
-    s_last = (prev == gridDim.x - 1);
-  }
+  if (tid == 0) s_last = arrive_last(p, participants);
   __syncthreads();
-  if (s_last) {
-    if (corpus && tid < nt) {
-      unsigned long long sum = 0;
-      for (int c = 0; c < kAccCopies; ++c) sum += atomicExch(&p.acc[c * nt + tid], 0ull);
-      s_tot[tid] = sum;
-      if (p.totals) p.totals[tid] = static_cast<int64_t>(sum);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      *p.err = atomicExch(p.ws_flag, 0);
-      *p.done = 0;
-    }
-    if (p.corpus && tid < 32) {
-      const int lane = tid;
-      warp_epilogue(lane < N ? static_cast<int64_t>(s_tot[lane]) : 0,
-                    lane < N ? static_cast<int64_t>(s_tot[N + lane]) : 0, static_cast<int64_t>(s_tot[2 * N]),
-                    static_cast<int64_t>(s_tot[2 * N + 1]), N, p.smoothing, p.eps, p.k,
-                    lane < N ? p.weights[lane] : 0.0, p.corpus + 2, p.corpus + 1, p.corpus);
-    }
-  }
+  if (s_last) finalize_launch(p, s_tot);
 }
 
 

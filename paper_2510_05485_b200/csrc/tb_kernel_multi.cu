@@ -76,12 +76,16 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
     mbar_init(mbar, 1);
   }
   griddep_wait_and_release();
-  if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x);
+  // list mode: the dense groups listed by the warp-per-group kernel before this one
+  const int64_t nb = p.glist ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned int*>(p.gcount)) : p.batch;
+  auto group_at = [&](int64_t i) -> int64_t { return p.glist ? static_cast<int64_t>(p.glist[i]) : i; };
+  if (static_cast<int64_t>(blockIdx.x) < nb) issue_stage(group_at(blockIdx.x));
   __syncthreads();
   TB_MARK(0);
   uint32_t phase = 0;
 
-  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+  for (int64_t gi = blockIdx.x; gi < nb; gi += gridDim.x) {
+    const int64_t b = group_at(gi);
     if (p.prefix_only) {
       __syncthreads();  // s_stage_len of this group, written by thread 0 in issue_rows
       if (tid <= R) s_len[tid] = s_stage_len[tid];
@@ -627,13 +631,13 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         }
       }
     }
-    if (b + gridDim.x < p.batch) {
+    if (gi + gridDim.x < nb) {
       __syncthreads();
-      issue_stage(b + gridDim.x);
+      issue_stage(group_at(gi + gridDim.x));
     }
     TB_MARK(30);
   }
-  finish_cta(p, s_tot, s_flags, s_last);
+  finish_cta(p, s_tot, s_flags, s_last, nb);
   TB_MARK(31);
 }
 

@@ -71,13 +71,19 @@ __global__ void __launch_bounds__(kThreads, 4)
     if (dbuf) mbar_init(mbars + 1, 1);
   }
   griddep_wait_and_release();
-  if (static_cast<int64_t>(blockIdx.x) < p.batch) issue_stage(blockIdx.x, 0);
+  // list mode: the dense groups listed by the warp-per-group kernel before this one
+  const int64_t nb = p.glist ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned int*>(p.gcount)) : p.batch;
+  auto group_at = [&](int64_t i) -> int64_t { return p.glist ? static_cast<int64_t>(p.glist[i]) : i; };
+  if (static_cast<int64_t>(blockIdx.x) < nb) issue_stage(group_at(blockIdx.x), 0);
   __syncthreads();
   TB_MARK(0);
   uint32_t phases = 0;  // bit i: parity of mbarrier i
-  bool try_filter = true;  // off after a group of this CTA needed the hash passes (related text)
+  // off after a group of this CTA needed the hash passes (related text); listed
+  // groups are known to need them
+  bool try_filter = p.glist == nullptr;
 
-  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+  for (int64_t gi = blockIdx.x; gi < nb; gi += gridDim.x) {
+    const int64_t b = group_at(gi);
     tok = tokb[cur];
     kc = reinterpret_cast<uint32_t*>(tok);
     if (p.prefix_only) {
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     phases ^= 1u << cur;
     __syncthreads();
     // every thread is past the previous group: its buffer takes the next group
-    if (dbuf && b + gridDim.x < p.batch) issue_stage(b + gridDim.x, cur ^ 1);
+    if (dbuf && gi + gridDim.x < nb) issue_stage(group_at(gi + gridDim.x), cur ^ 1);
     TB_MARK(2);
 
     const int clen = static_cast<int>(s_len[0]);
@@ -722,9 +728,9 @@ __global__ void __launch_bounds__(kThreads, 4)
         }
       }
     }
-    if (!dbuf && b + gridDim.x < p.batch) {
+    if (!dbuf && gi + gridDim.x < nb) {
       __syncthreads();
-      issue_stage(b + gridDim.x, 0);
+      issue_stage(group_at(gi + gridDim.x), 0);
     }
     if (dbuf) {
       cur ^= 1;
@@ -732,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
     TB_MARK(30);
   }
-  finish_cta(p, s_tot, s_flags, s_last);
+  finish_cta(p, s_tot, s_flags, s_last, nb);
   TB_MARK(31);
 }
 

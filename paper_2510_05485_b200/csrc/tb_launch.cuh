@@ -19,6 +19,10 @@ struct Plan {
   int ref_off[TB_MAX_REFS + 1] = {0};
   int off_id1 = 0, off_idn = 0, off_live = 0, off_ent = 0, off_mref = 0, off_kc = 0, off_lists = 0, off_seg = 0;
   int off_tok2 = 0;
+  // warp-per-group kernel first (R <= kSparseMaxRefs); the pair / multi kernel
+  // then scores the groups it lists, at workspace offset list_off
+  bool sparse = false;
+  size_t list_off = 0;
   size_t smem_bytes = 0;   // dynamic smem (smem mode)
   size_t gtab_stride = 0;  // per-CTA table bytes (global mode)
   int64_t grid = 0;
@@ -36,10 +40,15 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
                   size_t* attr_set, cudaStream_t stream, int threads = kThreads) {
   int dev = 0;
   TB_CUDA(cudaGetDevice(&dev));
-  if (pl.smem_bytes > 48 * 1024 && attr_set[dev & 63] < pl.smem_bytes) {
-    TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(pl.smem_bytes)));
-    attr_set[dev & 63] = pl.smem_bytes;
+  if (attr_set[dev & 63] < pl.smem_bytes + 1) {
+    if (pl.smem_bytes > 48 * 1024)
+      TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(pl.smem_bytes)));
+    // one shared-memory carveout for every stats kernel (no reconfiguration
+    // between back-to-back launches of different kernels)
+    TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    attr_set[dev & 63] = pl.smem_bytes + 1;
   }
   int64_t grid = pl.grid;
   if (persistent_fill) {
@@ -68,13 +77,16 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  // list mode (after the filter kernel): plain stream order — measured: with
+  // programmatic serialization the hash-table kernel ran 1.6x slower behind it
+  cfg.numAttrs = (no_pdl() || (prm.glist && pdl_mode() != 1)) ? 0 : 1;
   TB_CUDA(cudaLaunchKernelEx(&cfg, kern, prm));
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }
 
 // per-kernel launchers (one translation unit each); token_bytes 4 or 8
+int launch_sparse(const StatsParams& prm, int sms, cudaStream_t stream, int token_bytes);
 int launch_pair(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes);
 int launch_multi(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes);
 int launch_group(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes);

@@ -125,6 +125,42 @@ int cap_log2_for(int64_t want, int min_log2) {
   return c;
 }
 
+// The warp-per-group kernel goes first when the rows are narrow enough; the
+// CTA-per-group plan already made scores the groups it lists (a count and B
+// int32 group indices after the completion region).  TB_NO_SPARSE=1 turns it
+// off (A/B measurements).
+void use_sparse(Plan* pl, int64_t batch, int R, int64_t cand_width, const int64_t* ref_widths, int token_bytes,
+                int smem_optin) {
+  static const bool off = [] {
+    const char* e = getenv("TB_NO_SPARSE");
+    return e && e[0] == '1';
+  }();
+  static const bool force = [] {
+    const char* e = getenv("TB_FORCE_SPARSE");
+    return e && e[0] == '1';
+  }();
+  if (off || R > kSparseMaxRefs || cand_width > kSparseMaxWidth || batch > INT32_MAX) return;
+  // Measured on B200: the filter kernel wins for long rows in
+  // many waves (c5 2048-token rows: 263 -> 194 us); for <= 1024-token rows the
+  // hash-table kernel alone is as fast or faster (c4 37.6 vs 41.5 us with the
+  // list handoff; c2 7.5 vs 13.5 us), so it keeps them.  TB_FORCE_SPARSE=1
+  // takes the filter kernel for every shape (tests, A/B runs).
+  if (!force && (cand_width <= 1024 || batch < 8 * 148)) return;
+  // one group slot (tb_kernel_sparse.cu launch_sparse) must fit with room to spare
+  int64_t fc = 4096;  // Fc bytes: >= 16 per candidate position (tb_kernel_sparse.cu launch_sparse)
+  while (fc < 16 * cand_width) fc *= 2;
+  int64_t slot = fc + 2048 + 128 * token_bytes + 512 + 896 + 1024;
+  for (int s = 0; s <= R; ++s) {
+    const int64_t w = s == 0 ? cand_width : ref_widths[s - 1];
+    if (w > kSparseMaxWidth) return;
+    slot += (w * token_bytes + 16 + 15) / 16 * 16;
+  }
+  if (slot > smem_optin - 8192) return;
+  pl->sparse = true;
+  pl->list_off = pl->acc_bytes;
+  pl->ws_bytes = pl->acc_bytes + static_cast<size_t>(round_up(16 + 4 * batch, 256));
+}
+
 int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_widths, int token_bytes,
               int N, int smem_optin, int sms, Plan* pl) {
   (void)N;
@@ -206,6 +242,7 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
         pl->smem_bytes = static_cast<size_t>(total + tok2);
       }
       pl->ws_bytes = pl->acc_bytes;
+      use_sparse(pl, batch, R, cand_width, ref_widths, token_bytes, smem_optin);
       return TB_OK;
     }
   }
@@ -260,6 +297,7 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
       pl->off_lists = static_cast<int>(offs[5]);
       pl->smem_bytes = static_cast<size_t>(total);
       pl->ws_bytes = pl->acc_bytes;
+      use_sparse(pl, batch, R, cand_width, ref_widths, token_bytes, smem_optin);
       return TB_OK;
     }
   }
@@ -335,6 +373,16 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
 }
 
 int launch_stats(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes) {
+  if (pl.sparse) {  // warp per group; then the listed dense groups, CTA per group
+    const int rc = launch_sparse(prm, sms, stream, token_bytes);
+    if (rc != TB_OK) return rc;
+    // TB_DEBUG_NO_DENSE=1: timing experiments only (results are wrong if a group was listed)
+    static const bool no_dense = [] {
+      const char* e = getenv("TB_DEBUG_NO_DENSE");
+      return e && e[0] == '1';
+    }();
+    if (no_dense) return TB_OK;
+  }
   if (pl.pair) return launch_pair(prm, pl, sms, stream, token_bytes);
   if (pl.multi) return launch_multi(prm, pl, sms, stream, token_bytes);
   if (pl.smem_mode) return launch_group(prm, pl, sms, stream, token_bytes);
@@ -452,6 +500,10 @@ static int stats_impl(int32_t token_bytes, const void* cand_ids, int64_t cand_ld
   prm.gtab_stride = pl.gtab_stride;
   prm.prefix_only = prefix_only && pl.smem_mode;
   prm.err_store = err_store;
+  if (pl.sparse) {
+    prm.gcount = reinterpret_cast<unsigned int*>(ws + pl.list_off);
+    prm.glist = reinterpret_cast<int*>(ws + pl.list_off + 16);
+  }
 
   return launch_stats(prm, pl, d->sms, stream, token_bytes);
 }
@@ -863,8 +915,20 @@ int host_pipelined(HostCtx& c, int token_bytes, int R, const void* const* ids, c
   }
   rc = grow_pinned_rows(c, chunk_bytes * nchunks);
   if (rc != TB_OK) return rc;
-  rc = grow_device(&c.ws, &c.ws_bytes, kAccBytes, true);  // the shared-memory plans need the completion region only
-  if (rc != TB_OK) return rc;
+  {  // the shared-memory plans need the completion region (+ the dense-group list)
+    size_t want = kAccBytes;
+    DevInfo* d = nullptr;
+    rc = dev_info(&d);
+    if (rc != TB_OK) return rc;
+    for (int tbytes = 4; tbytes <= 8; tbytes += 4) {
+      Plan cp;
+      if (make_plan(rows_per, R, widths[0], widths + 1, tbytes, N, d->smem_optin, d->sms, &cp) == TB_OK &&
+          cp.ws_bytes > want)
+        want = cp.ws_bytes;
+    }
+    rc = grow_device(&c.ws, &c.ws_bytes, want, true);
+    if (rc != TB_OK) return rc;
+  }
   int32_t* err_host = reinterpret_cast<int32_t*>(c.pin);
   for (int i = 0; i < nchunks; ++i) err_host[i] = 0;
   auto P = [&](int i, int64_t b0) -> void* {
