@@ -189,6 +189,15 @@ int tb_validate_batch(int32_t token_bytes, const void* ids, int64_t ld, int64_t 
                       const int64_t* lengths, int64_t batch, int32_t* err_flag,
                       void* stream);
 
+/* The same validation for a HOST batch (numpy / torch CPU arrays), run on the
+ * library's host threads — `TokenBatch.__post_init__` (batch.py:25-35) without
+ * the per-element numpy masks.  Returns TB_FLAG_BAD_LENGTH when a length lies
+ * outside [0, width] (checked first, as the reference does), else
+ * TB_FLAG_NEGATIVE_ID when a valid position holds a negative ID, else 0;
+ * -TB_ERR_* on an argument error.  Reads host memory only (no GPU needed). */
+int tb_validate_host(int32_t token_bytes, const void* ids, int64_t ld, int64_t width,
+                     const int64_t* lengths, int64_t batch);
+
 /* ------------------------------------------------------------------------ *
  *  Reference operator/plugin surface (_backend.py:45-54) on the device      *
  * ------------------------------------------------------------------------ */

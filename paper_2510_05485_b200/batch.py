@@ -114,14 +114,17 @@ class TokenBatch:
 
     def _row_view(self, want64: bool):
         """(ids pointer, ld, width, lengths pointer, token bytes) of this batch
-        for the C ABI, plus the arrays that keep those pointers alive.  Cached
-        (the batch is immutable); int32 IDs are widened once when `want64`
-        (batches of one call must share a token width)."""
-        key = "_view64" if want64 else "_view"
-        v = self.__dict__.get(key)
+        for the C ABI, plus the arrays that keep those pointers alive.  The view
+        of the batch's own arrays is cached (they are read live on every call:
+        in-place writes to a trusted buffer are seen).  When `want64` widens
+        int32 IDs (batches of one call share a token width) the copy is made
+        per call and never cached, so it cannot go stale."""
+        ids, lengths = self.ids, self.lengths
+        widen = want64 and (ids.dtype != np.int64 if isinstance(ids, np.ndarray) else ids.dtype != torch.int64)
+        key = "_view"
+        v = None if widen else self.__dict__.get(key)
         if v is not None:
             return v
-        ids, lengths = self.ids, self.lengths
         if isinstance(ids, np.ndarray):
             if want64 and ids.dtype != np.int64:
                 ids = ids.astype(np.int64)
@@ -134,7 +137,8 @@ class TokenBatch:
             ld = ids.shape[1]
         lptr = lengths.ctypes.data if isinstance(lengths, np.ndarray) else lengths.data_ptr()
         v = ((ptr, ld, int(ids.shape[1]), lptr, isz), (ids, lengths))
-        object.__setattr__(self, key, v)
+        if not widen:
+            object.__setattr__(self, key, v)
         return v
 
     @property
@@ -186,14 +190,24 @@ class TokenBatch:
 
 
 def _validate_host(ids: np.ndarray, lengths: np.ndarray) -> None:
-    """batch.py:25-35."""
+    """batch.py:25-35: same checks, order and messages; the element checks run
+    in the native library on its host threads (tb_validate_host)."""
     if ids.ndim != 2:
         raise ValueError(f"ids must be 2-D, got shape {ids.shape}")
     if lengths.shape != (ids.shape[0],):
         raise ValueError(
             f"lengths shape {lengths.shape} does not match batch size {ids.shape[0]}")
-    if np.any(lengths < 0) or np.any(lengths > ids.shape[1]):
+    if ids.shape[0] == 0:
+        return
+    if ids.dtype not in (np.int32, np.int64) or not ids.flags.c_contiguous and ids.strides[1] != ids.itemsize:
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+    lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+    ld = ids.strides[0] // ids.itemsize if ids.shape[0] > 1 else ids.shape[1]
+    rc = _native.load().tb_validate_host(ids.itemsize, ids.ctypes.data, ld, ids.shape[1],
+                                         lengths.ctypes.data, ids.shape[0])
+    if rc < 0:
+        _native.check(-rc, "tb_validate_host")
+    if rc & _native.TB_FLAG_BAD_LENGTH:
         raise ValueError("lengths must lie in [0, max_len]")
-    valid = np.arange(ids.shape[1]) < lengths[:, None]
-    if ids.size and np.any(ids[valid] < 0):
+    if rc & _native.TB_FLAG_NEGATIVE_ID:
         raise ValueError("token IDs within valid positions must be non-negative")

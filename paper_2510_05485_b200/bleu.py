@@ -167,7 +167,8 @@ def _launch_host(candidates: TokenBatch, references: Sequence[TokenBatch], confi
     want64 = not candidates._tok32
     for b in references:
         want64 = want64 or not b._tok32
-    views = (candidates._row_view(want64)[0], *[b._row_view(want64)[0] for b in references])
+    held = [candidates._row_view(want64), *[b._row_view(want64) for b in references]]  # keeps widened copies alive
+    views = tuple(h[0] for h in held)
     smc, eps, k, waddr = _config_abi(config)
     rc, flags, *outs = hp.run(_MODES[mode], views, candidates.batch_size, config.max_order,
                               smc, eps, k, waddr, _native.raw_stream(dev))
@@ -199,7 +200,8 @@ def _launch_device(candidates: TokenBatch, references: Sequence[TokenBatch], con
     hp = _native.hostpath()
     batches = (candidates, *references)
     want64 = any(b.ids.dtype != torch.int32 for b in batches)
-    views = tuple(b._row_view(want64)[0] for b in batches)
+    held = [b._row_view(want64) for b in batches]  # widened copies live until the launch is queued
+    views = tuple(h[0] for h in held)
     B, N = candidates.batch_size, config.max_order
     key = (device.index, B, tuple(v[2] for v in views), views[0][4], N)
     wsb = _ws_bytes_cache.get(key)

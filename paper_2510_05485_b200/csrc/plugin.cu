@@ -13,6 +13,7 @@
 // plugin functions; the fused sentence path lives in tensorbleu.cu.
 
 #include "../../include/tensorbleu.h"
+#include "tb_guard.h"
 
 #include <cuda_runtime.h>
 
@@ -390,6 +391,7 @@ size_t tb_unique_rows_workspace_bytes(int64_t t, int32_t n) {
 
 int tb_unique_rows(const int64_t* rows, int64_t t, int32_t n, int64_t* unique_out, int64_t* inverse_out,
                    int64_t* num_unique, void* workspace, size_t workspace_bytes, void* stream_) {
+  StreamDeviceGuard device_guard(stream_);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (t < 0 || n < 0 || !num_unique) return TB_ERR_INVALID_ARG;
   if (t == 0) {
@@ -476,6 +478,7 @@ static int segment_common(bool clip, const int64_t* ids, int64_t num_ids, const 
 int tb_segment_bincount(const int64_t* ids, int64_t num_ids, const int64_t* seg_lengths, int64_t b,
                         int64_t num_unique, int32_t* counts_out, int32_t* err_flag, void* workspace,
                         size_t workspace_bytes, void* stream) {
+  StreamDeviceGuard device_guard(stream);
   return segment_common(false, ids, num_ids, seg_lengths, b, num_unique, counts_out, nullptr, nullptr,
                         err_flag, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
@@ -483,11 +486,13 @@ int tb_segment_bincount(const int64_t* ids, int64_t num_ids, const int64_t* seg_
 int tb_clipped_numerators(const int64_t* ids, int64_t num_ids, const int64_t* seg_lengths, int64_t b,
                           const int32_t* ref_max, int64_t num_unique, int64_t* num_out, int32_t* err_flag,
                           void* workspace, size_t workspace_bytes, void* stream) {
+  StreamDeviceGuard device_guard(stream);
   return segment_common(true, ids, num_ids, seg_lengths, b, num_unique, nullptr, ref_max, num_out, err_flag,
                         workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int tb_count_binary(const int32_t* a, const int32_t* b, int32_t* out, int64_t count, int32_t op, void* stream) {
+  StreamDeviceGuard device_guard(stream);
   if (count < 0 || (op != 0 && op != 1)) return TB_ERR_INVALID_ARG;
   if (count == 0) return TB_OK;
   if (!a || !b || !out) return TB_ERR_INVALID_ARG;

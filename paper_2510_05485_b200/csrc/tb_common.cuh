@@ -15,6 +15,7 @@
 #pragma once
 
 #include "../../include/tensorbleu.h"
+#include "tb_guard.h"
 
 #include <cuda_runtime.h>
 

@@ -526,7 +526,32 @@ struct HostCtx {
   unsigned char* rows_dev = nullptr;
   size_t rows_bytes = 0;
 };
-thread_local HostCtx g_host[64];
+// Host-call contexts: a per-device pool shared by all calling threads (a
+// call takes one for its duration and gives it back), so concurrent calls
+// get separate buffers and threads that exit leave nothing behind.
+struct HostPool {
+  std::mutex m;
+  std::vector<HostCtx*> free_list;
+};
+HostPool g_host_pool[64];
+
+struct HostLease {  // RAII: a context of device `dev` for one call
+  int dev;
+  HostCtx* c;
+  explicit HostLease(int d) : dev(d), c(nullptr) {
+    std::lock_guard<std::mutex> l(g_host_pool[dev].m);
+    auto& fl = g_host_pool[dev].free_list;
+    if (!fl.empty()) {
+      c = fl.back();
+      fl.pop_back();
+    }
+    if (!c) c = new HostCtx();
+  }
+  ~HostLease() {
+    std::lock_guard<std::mutex> l(g_host_pool[dev].m);
+    g_host_pool[dev].free_list.push_back(c);
+  }
+};
 
 int grow_device(void** buf, size_t* have, size_t want, bool zero) {
   if (*have >= want && *buf) return TB_OK;
@@ -603,9 +628,14 @@ class CopyPool {
   }
 
  private:
+  // TB_COPY_THREADS: worker threads (default min(7, cores/2 - 1));
+  // TB_COPY_SPIN_US: how long an idle worker spins for the next job before it
+  // sleeps (default 200 us; calls usually come back to back)
   CopyPool() {
     const unsigned hw = std::thread::hardware_concurrency();
-    const int nt = std::max(0, std::min(7, static_cast<int>(hw / 2) - 1));
+    int nt = std::max(0, std::min(7, static_cast<int>(hw / 2) - 1));
+    if (const char* e = getenv("TB_COPY_THREADS")) nt = std::max(0, std::min(64, atoi(e)));
+    if (const char* e = getenv("TB_COPY_SPIN_US")) spin_us_ = std::max(0, atoi(e));
     for (int i = 0; i < nt; ++i) threads_.emplace_back([this] { loop(); });
   }
   ~CopyPool() {
@@ -635,7 +665,12 @@ class CopyPool {
       // condition-variable wake-up costs tens of microseconds), then sleep
       const auto t0 = std::chrono::steady_clock::now();
       while (gen_pub_.load() == seen && !stop_flag_.load() &&
-             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(300)) {
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(spin_us_)) {
+#if defined(__x86_64__) || defined(__i386__)
+        __builtin_ia32_pause();
+#else
+        std::this_thread::yield();
+#endif
       }
       uint32_t g;
       std::function<void(int)>* fn;
@@ -652,6 +687,7 @@ class CopyPool {
     }
   }
   std::vector<std::thread> threads_;
+  int spin_us_ = 200;
   std::mutex job_, m_;
   std::condition_variable cv_;
   // the current job (written under m_)
@@ -850,6 +886,7 @@ int tb_bleu_stats(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, in
                   int64_t* eff_ref_out, double* scores_out, double* precisions_out, double* bp_out,
                   int64_t* totals_out, double* corpus_out, int32_t* err_flag, void* workspace,
                   size_t workspace_bytes, void* stream) {
+  StreamDeviceGuard device_guard(stream);
   return stats_impl(token_bytes, cand_ids, cand_ld, cand_width, cand_len, num_refs, ref_ids, ref_ld, ref_width,
                     ref_len, batch, max_order, smoothing, eps, k, weights, num_out, den_out, cand_len_out,
                     eff_ref_out, scores_out, precisions_out, bp_out, totals_out, corpus_out, err_flag, workspace,
@@ -979,6 +1016,7 @@ int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int
                  const double* weights, int64_t* num_out, int64_t* den_out, int64_t* cand_len_out,
                  int64_t* eff_ref_out, double* scores_out, double* precisions_out, double* bp_out,
                  int64_t* totals_out, double* corpus_out, int32_t* flags_out, void* stream_) {
+  StreamDeviceGuard device_guard(stream_);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (token_bytes != 4 && token_bytes != 8) return TB_ERR_INVALID_ARG;
   if (num_refs < 1) return TB_ERR_INVALID_ARG;
@@ -997,7 +1035,8 @@ int tb_bleu_host(int32_t token_bytes, const void* cand_ids, int64_t cand_ld, int
   int dev = 0;
   TB_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return TB_ERR_UNSUPPORTED;
-  HostCtx& c = g_host[dev];
+  HostLease lease(dev);
+  HostCtx& c = *lease.c;
   DevInfo* d = nullptr;
   rc = dev_info(&d);
   if (rc != TB_OK) return rc;
@@ -1139,6 +1178,7 @@ int tb_bleu_scores(const int64_t* num, const int64_t* den, const int64_t* cand_l
                    const int64_t* eff_ref, int64_t batch, int32_t max_order, int32_t smoothing,
                    double eps, double k, const double* weights, double* scores_out,
                    double* precisions_out, double* bp_out, void* stream) {
+  StreamDeviceGuard device_guard(stream);
   int rc = check_epi(max_order, smoothing, eps, k, weights);
   if (rc != TB_OK) return rc;
   if (batch < 0) return TB_ERR_INVALID_ARG;
@@ -1158,6 +1198,7 @@ int tb_bleu_scores(const int64_t* num, const int64_t* den, const int64_t* cand_l
 int tb_bleu_totals(const int64_t* num, const int64_t* den, const int64_t* cand_len,
                    const int64_t* eff_ref, int64_t batch, int32_t max_order, int64_t* totals_out,
                    void* stream) {
+  StreamDeviceGuard device_guard(stream);
   if (max_order < 1) return TB_ERR_INVALID_ARG;
   if (max_order > TB_MAX_ORDER) return TB_ERR_UNSUPPORTED;
   if (batch < 0 || !totals_out) return TB_ERR_INVALID_ARG;
@@ -1168,8 +1209,53 @@ int tb_bleu_totals(const int64_t* num, const int64_t* den, const int64_t* cand_l
   return TB_OK;
 }
 
+int tb_validate_host(int32_t token_bytes, const void* ids, int64_t ld, int64_t width, const int64_t* lengths,
+                     int64_t batch) {
+  if (token_bytes != 4 && token_bytes != 8) return -TB_ERR_INVALID_ARG;
+  if (batch < 0 || width < 0 || ld < width) return -TB_ERR_INVALID_ARG;
+  if (batch == 0) return 0;
+  if (!lengths || (!ids && width > 0)) return -TB_ERR_INVALID_ARG;
+  for (int64_t b = 0; b < batch; ++b)  // batch.py:30-31, checked first
+    if (lengths[b] < 0 || lengths[b] > width) return TB_FLAG_BAD_LENGTH;
+  // batch.py:32-34: the OR of the valid IDs of a block of rows has its sign
+  // bit set iff one of them is negative
+  auto rows_negative = [&](int64_t r0, int64_t r1) -> bool {
+    if (token_bytes == 8) {
+      const int64_t* p = static_cast<const int64_t*>(ids);
+      for (int64_t b = r0; b < r1; ++b) {
+        const int64_t* row = p + b * ld;
+        int64_t acc = 0;
+        for (int64_t j = 0; j < lengths[b]; ++j) acc |= row[j];
+        if (acc < 0) return true;
+      }
+    } else {
+      const int32_t* p = static_cast<const int32_t*>(ids);
+      for (int64_t b = r0; b < r1; ++b) {
+        const int32_t* row = p + b * ld;
+        int32_t acc = 0;
+        for (int64_t j = 0; j < lengths[b]; ++j) acc |= row[j];
+        if (acc < 0) return true;
+      }
+    }
+    return false;
+  };
+  int64_t tokens = 0;
+  for (int64_t b = 0; b < batch; ++b) tokens += lengths[b];
+  if (tokens < (int64_t(1) << 16)) return rows_negative(0, batch) ? TB_FLAG_NEGATIVE_ID : 0;
+  constexpr int64_t kRows = 32;
+  const int64_t items = (batch + kRows - 1) / kRows;
+  std::atomic<int> neg{0};
+  CopyPool::get().run(static_cast<int>(items), [&](int item) {
+    if (neg.load(std::memory_order_relaxed)) return;
+    const int64_t r0 = item * kRows;
+    if (rows_negative(r0, std::min(batch, r0 + kRows))) neg.store(1, std::memory_order_relaxed);
+  });
+  return neg.load() ? TB_FLAG_NEGATIVE_ID : 0;
+}
+
 int tb_validate_batch(int32_t token_bytes, const void* ids, int64_t ld, int64_t width,
                       const int64_t* lengths, int64_t batch, int32_t* err_flag, void* stream_) {
+  StreamDeviceGuard device_guard(stream_);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   if (token_bytes != 4 && token_bytes != 8) return TB_ERR_INVALID_ARG;
   if (batch < 0 || width < 0 || ld < width || !err_flag) return TB_ERR_INVALID_ARG;

@@ -6,10 +6,12 @@ pkg/bindings/src/batchbleu_ext/_ext.pyx:1-110).
 (B, L) for a single reference set, ``ref_lengths`` (R, B) or (B,).  Same
 dimension-naming errors as the reference.
 
-Differences, both in the caller's favour: CUDA tensors are accepted
-zero-copy (DLPack-free: torch tensors as-is), and int32 token buffers are
-NOT widened — the kernels read int32 natively — so only int32 *lengths*
-count as layout copies.
+Host arrays follow the reference exactly: every buffer becomes C-contiguous
+int64 and each conversion counts as one copy (``copy_count``, _ext.pyx:31-46;
+int32 inputs cost four).  In addition, torch tensors (host or CUDA) are used
+as they are — int32 token tensors are read natively by the kernels, CUDA
+tensors zero-copy — and only a non-contiguous tensor or non-int64 lengths
+count as copies.
 """
 
 from __future__ import annotations
@@ -49,12 +51,14 @@ def _as_tokens(name, buf, expected_ndim):
         raise TypeError(f"{name} must be int32 or int64, got {arr.dtype}")
     if arr.ndim != expected_ndim:
         raise ValueError(f"{name} must have {expected_ndim} dimensions, got {arr.ndim}")
-    if isinstance(arr, torch.Tensor):
+    if isinstance(arr, torch.Tensor):  # int32 / int64 tensors are used as they are
         if not arr.is_contiguous():
             _copy_count += 1
             arr = arr.contiguous()
         return arr
-    out = np.ascontiguousarray(arr)
+    # host arrays: C-contiguous int64, as TokenBatch holds them (batch.py:23) —
+    # int32 arrays are widened here, with the copy counted (_ext.pyx:31-46)
+    out = np.ascontiguousarray(arr, dtype=np.int64)
     if out is not arr:
         _copy_count += 1
     return out
