@@ -202,6 +202,19 @@ int tb_validate_host(int32_t token_bytes, const void* ids, int64_t ld, int64_t w
  *  Reference operator/plugin surface (_backend.py:45-54) on the device      *
  * ------------------------------------------------------------------------ */
 
+/* Workspace bytes for tb_flatten_windows over `batch` rows. */
+size_t tb_windows_workspace_bytes(int64_t batch);
+
+/* Replaces `extract_ngrams` + `flatten_valid` (ngrams.py:63-83): the valid
+ * order-n windows of every row (row i contributes max(len_i - n + 1, 0),
+ * lengths clamped to [0, width]) concatenated row-major into out (T, n)
+ * int64, T written to *total_out (device).  `out` must hold the upper bound
+ * batch * max(width - n + 1, 0) rows.  ids device (batch, ld) int32|int64;
+ * lengths device (batch,) int64. */
+int tb_flatten_windows(int32_t token_bytes, const void* ids, int64_t ld, int64_t width,
+                       const int64_t* lengths, int64_t batch, int32_t n, int64_t* out,
+                       int64_t* total_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Workspace bytes for tb_unique_rows on t rows of n columns. */
 size_t tb_unique_rows_workspace_bytes(int64_t t, int32_t n);
 

@@ -68,10 +68,10 @@ def unique_rows(rows):
     """Deduplicate the rows of a (T, n) int64 array (_backend.py:45-46,
     _kernels.pyx:36-81).
 
-    Returns (unique (U, n), inverse (T,)).  Unique rows come out in
-    first-occurrence order (the reference backends sort lexicographically;
-    SPEC.md leaves the order implementation-defined and only the
-    reconstruction invariant unique[inverse] == rows is contractual)."""
+    Returns (unique (U, n), inverse (T,)), identical to the reference
+    backends: unique rows in lexicographic order (signed int64), inverse the
+    rank of each row's group (device: a hash dictionary, then an LSD radix
+    sort of the unique rows, plugin.cu)."""
     lib = _native.load()
     host, device = _device_for(rows)
     if not isinstance(rows, torch.Tensor):

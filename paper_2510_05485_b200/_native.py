@@ -76,6 +76,8 @@ SIGNATURES = {
     "tb_bleu_totals": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _P]),
     "tb_validate_batch": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64, _P, _P]),
     "tb_validate_host": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64]),
+    "tb_windows_workspace_bytes": (_SZ, [_I64]),
+    "tb_flatten_windows": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64, _I32, _P, _P, _P, _SZ, _P]),
     "tb_unique_rows_workspace_bytes": (_SZ, [_I64, _I32]),
     "tb_unique_rows": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _SZ, _P]),
     "tb_segment_workspace_bytes": (_SZ, [_I64, _I64]),

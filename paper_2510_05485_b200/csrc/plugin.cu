@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 #include <cstdio>
@@ -162,6 +163,41 @@ struct OffsetSink {
 };
 
 // --------------------------------------------------------------------------
+// Valid n-gram windows (extract_ngrams + flatten_valid, ngrams.py:63-83):
+// row i contributes max(len_i - n + 1, 0) windows, concatenated row-major.
+// --------------------------------------------------------------------------
+struct WindowCount {
+  const int64_t* len;
+  int64_t width;
+  int n;
+  __device__ long long operator()(int64_t i) const {
+    int64_t l = len[i];
+    l = l < 0 ? 0 : (l > width ? width : l);
+    const int64_t c = l - n + 1;
+    return c > 0 ? c : 0;
+  }
+};
+
+// one warp per row: window j of row i -> out[(off_i + j) * n + c] = ids[i, j + c]
+template <typename T>
+__global__ void __launch_bounds__(256) windows_fill_kernel(const T* __restrict__ ids, int64_t ld, int64_t batch,
+                                                           int n, WindowCount cnt, const int64_t* __restrict__ off,
+                                                           int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < batch;
+       i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t c = cnt(i);
+    const T* row = ids + i * ld;
+    int64_t* dst = out + off[i] * n;
+    // element e of this row's output block is column e % n of window e / n
+    for (int64_t e = lane; e < c * n; e += 32) {
+      const int64_t j = e / n, col = e - j * n;
+      dst[e] = static_cast<int64_t>(row[j + col]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // Dictionary (unique_rows).
 // --------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t row_hash(const int64_t* row, int n) {
@@ -228,6 +264,147 @@ __global__ void dict_finalize_kernel(int64_t* inverse, int64_t t, const int64_t*
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < t;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     inverse[i] = id_of_slot[inverse[i]];
+}
+
+// --------------------------------------------------------------------------
+// Lexicographic order of the unique rows (the reference sorts rows
+// lexicographically as signed int64, _kernels.pyx:20-30 / _py_kernels.py:24):
+// an LSD radix sort of the U unique rows' indices — columns from last to first,
+// 8-bit digits of the sign-flipped key from least to most significant, every
+// pass stable — then the unique rows are gathered in that order and the
+// inverse indices renumbered.  U is device-resident (no host round trip).
+// --------------------------------------------------------------------------
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 4;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;
+constexpr uint64_t kSignFlip = 0x8000000000000000ull;
+
+__device__ __forceinline__ int64_t used_tiles(const int64_t* u) { return (*u + kRadixTile - 1) / kRadixTile; }
+
+// keys[j] = column `col` of unique row perm[j] (perm = identity when init)
+__global__ void lex_keys_kernel(const int64_t* __restrict__ uniq, int n, int col, int64_t* perm, bool init,
+                                uint64_t* __restrict__ keys, const int64_t* __restrict__ num_unique) {
+  const int64_t u = *num_unique;
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < u;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (init) perm[j] = j;
+    keys[j] = static_cast<uint64_t>(uniq[perm[j] * n + col]) ^ kSignFlip;
+  }
+}
+
+// per tile: counts of each digit -> ghist[digit * ntiles + tile]
+__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint64_t* __restrict__ keys,
+                                                                   const int64_t* __restrict__ num_unique,
+                                                                   int shift, uint32_t* ghist, int64_t ntiles) {
+  __shared__ uint32_t h[256];
+  const int64_t tile = blockIdx.x;
+  if (tile >= used_tiles(num_unique)) return;
+  const int64_t u = *num_unique;
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int k = 0; k < kRadixItems; ++k) {
+    const int64_t j = tile * kRadixTile + k * kRadixThreads + threadIdx.x;
+    if (j < u) atomicAdd(&h[(keys[j] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  ghist[threadIdx.x * ntiles + tile] = h[threadIdx.x];
+}
+
+// exclusive scan of one digit's tile counts (block d), and the digit's total
+__global__ void __launch_bounds__(kRadixThreads) radix_scan_kernel(uint32_t* ghist, int64_t ntiles,
+                                                                   const int64_t* __restrict__ num_unique,
+                                                                   uint32_t* dtotal) {
+  __shared__ uint32_t s[kRadixThreads];
+  const int d = blockIdx.x;
+  const int64_t nt = used_tiles(num_unique);
+  uint32_t carry = 0;
+  for (int64_t base = 0; base < nt; base += kRadixThreads) {
+    const int64_t t = base + threadIdx.x;
+    const uint32_t v = t < nt ? ghist[d * ntiles + t] : 0u;
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < kRadixThreads; off <<= 1) {  // inclusive Hillis-Steele scan
+      const uint32_t x = threadIdx.x >= off ? s[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s[threadIdx.x] += x;
+      __syncthreads();
+    }
+    if (t < nt) ghist[d * ntiles + t] = carry + s[threadIdx.x] - v;
+    carry += s[kRadixThreads - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dtotal[d] = carry;
+}
+
+// stable scatter of one tile: destination = digit base + this tile's offset
+// within the digit + rank among the tile's elements of that digit (in order)
+__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
+    const uint64_t* __restrict__ kin, const int64_t* __restrict__ pin, uint64_t* __restrict__ kout,
+    int64_t* __restrict__ pout, const int64_t* __restrict__ num_unique, int shift, const uint32_t* __restrict__ ghist,
+    int64_t ntiles, const uint32_t* __restrict__ dtotal) {
+  __shared__ uint32_t s_base[256], s_run[256], s_scan[256];
+  __shared__ uint32_t s_w[kRadixThreads / 32][256];
+  const int64_t tile = blockIdx.x;
+  if (tile >= used_tiles(num_unique)) return;
+  const int64_t u = *num_unique;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // digit bases: exclusive scan of the digit totals
+  const uint32_t tot = dtotal[tid];
+  s_scan[tid] = tot;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {
+    const uint32_t x = tid >= off ? s_scan[tid - off] : 0u;
+    __syncthreads();
+    s_scan[tid] += x;
+    __syncthreads();
+  }
+  s_base[tid] = s_scan[tid] - tot + ghist[tid * ntiles + tile];
+  s_run[tid] = 0;
+  for (int k = 0; k < kRadixItems; ++k) {
+    const int64_t j = tile * kRadixTile + k * kRadixThreads + tid;
+    const bool valid = j < u;
+    const uint64_t key = valid ? kin[j] : 0ull;
+    const uint32_t d = valid ? static_cast<uint32_t>((key >> shift) & 255u) : 256u + lane;
+#pragma unroll
+    for (int w = 0; w < kRadixThreads / 32; ++w) s_w[w][tid] = 0;
+    __syncthreads();
+    const unsigned peers = __match_any_sync(kFull, d);
+    const int lrank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && lrank == 0) s_w[warp][d] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      uint32_t prefix = 0;
+      for (int w = 0; w < warp; ++w) prefix += s_w[w][d];
+      const uint32_t pos = s_base[d] + s_run[d] + prefix + static_cast<uint32_t>(lrank);
+      kout[pos] = key;
+      pout[pos] = pin[j];
+    }
+    __syncthreads();
+    uint32_t add = 0;
+#pragma unroll
+    for (int w = 0; w < kRadixThreads / 32; ++w) add += s_w[w][tid];
+    s_run[tid] += add;
+    __syncthreads();
+  }
+}
+
+// rank[perm[k]] = k; unique rows in sorted order
+__global__ void lex_gather_kernel(const int64_t* __restrict__ uniq_fo, int n, const int64_t* __restrict__ perm,
+                                  int64_t* __restrict__ rank, int64_t* __restrict__ unique_out,
+                                  const int64_t* __restrict__ num_unique) {
+  const int64_t u = *num_unique;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < u;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t src = perm[k];
+    rank[src] = k;
+    for (int c = 0; c < n; ++c) unique_out[k * n + c] = uniq_fo[src * n + c];
+  }
+}
+
+__global__ void lex_inverse_kernel(int64_t* inverse, int64_t t, const int64_t* __restrict__ rank) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < t;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    inverse[i] = rank[inverse[i]];
 }
 
 // --------------------------------------------------------------------------
@@ -381,12 +558,53 @@ size_t segment_ws(int64_t b) {
 
 extern "C" {
 
+size_t tb_windows_workspace_bytes(int64_t batch) {
+  const int64_t nb = (batch + kTile - 1) / kTile;
+  return static_cast<size_t>(round_up((batch + 1) * 8, 256) + round_up((nb + 1) * 8, 256) + 256);
+}
+
+int tb_flatten_windows(int32_t token_bytes, const void* ids, int64_t ld, int64_t width, const int64_t* lengths,
+                       int64_t batch, int32_t n, int64_t* out, int64_t* total_out, void* workspace,
+                       size_t workspace_bytes, void* stream_) {
+  StreamDeviceGuard device_guard(stream_);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if ((token_bytes != 4 && token_bytes != 8) || batch < 0 || width < 0 || ld < width || n < 1 || !total_out)
+    return TB_ERR_INVALID_ARG;
+  if (batch == 0) {
+    TB_CUDA(cudaMemsetAsync(total_out, 0, sizeof(int64_t), stream));
+    return TB_OK;
+  }
+  if (!lengths || (!ids && width > 0) || !out) return TB_ERR_INVALID_ARG;
+  if (workspace_bytes < tb_windows_workspace_bytes(batch) || !workspace) return TB_ERR_WORKSPACE;
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  auto* off = reinterpret_cast<int64_t*>(ws);
+  auto* bsum = reinterpret_cast<int64_t*>(ws + round_up((batch + 1) * 8, 256));
+  const int64_t nb = (batch + kTile - 1) / kTile;
+  WindowCount cnt{lengths, width, n};
+  tile_sum_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, stream>>>(cnt, batch, bsum);
+  scan_bsums_kernel<<<1, kScanThreads, 0, stream>>>(bsum, nb, total_out);
+  tile_scan_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, stream>>>(cnt, batch, bsum, OffsetSink{off});
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((batch + 7) / 8, 4 * num_sms() * 8));
+  if (token_bytes == 4)
+    windows_fill_kernel<int32_t><<<grid, 256, 0, stream>>>(static_cast<const int32_t*>(ids), ld, batch, n, cnt,
+                                                            off, out);
+  else
+    windows_fill_kernel<int64_t><<<grid, 256, 0, stream>>>(static_cast<const int64_t*>(ids), ld, batch, n, cnt,
+                                                            off, out);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
 size_t tb_unique_rows_workspace_bytes(int64_t t, int32_t n) {
-  (void)n;
   int64_t cap = 32;
   while (cap < 2 * t) cap <<= 1;
   const int64_t nb = (t + kTile - 1) / kTile;
-  return static_cast<size_t>(3 * round_up(cap * 8, 256) + round_up((nb + 1) * 8, 256) + 256);
+  const int64_t nt = (t + kRadixTile - 1) / kRadixTile;
+  // hash table (keys, representatives, ids) + tile sums, then the sort:
+  // first-occurrence unique rows, keys x2, permutation x2, ranks, histograms
+  return static_cast<size_t>(3 * round_up(cap * 8, 256) + round_up((nb + 1) * 8, 256) + 256 +
+                             round_up(t * (n > 0 ? n : 1) * 8, 256) + 5 * round_up(t * 8, 256) +
+                             round_up(256 * nt * 4, 256) + 256 * 4 + 256);
 }
 
 int tb_unique_rows(const int64_t* rows, int64_t t, int32_t n, int64_t* unique_out, int64_t* inverse_out,
@@ -409,6 +627,24 @@ int tb_unique_rows(const int64_t* rows, int64_t t, int32_t n, int64_t* unique_ou
   auto* bsum = reinterpret_cast<int64_t*>(ws + 3 * round_up(cap * 8, 256));
   const int64_t nb = (t + kTile - 1) / kTile;
 
+  // the sort's buffers after the hash table
+  unsigned char* q = ws + 3 * round_up(cap * 8, 256) + round_up((nb + 1) * 8, 256) + 256;
+  auto take = [&](int64_t bytes) {
+    unsigned char* r = q;
+    q += round_up(bytes, 256);
+    return r;
+  };
+  auto* uniq_fo = reinterpret_cast<int64_t*>(take(t * (n > 0 ? n : 1) * 8));
+  auto* keys_a = reinterpret_cast<uint64_t*>(take(t * 8));
+  auto* keys_b = reinterpret_cast<uint64_t*>(take(t * 8));
+  auto* perm_a = reinterpret_cast<int64_t*>(take(t * 8));
+  auto* perm_b = reinterpret_cast<int64_t*>(take(t * 8));
+  auto* rank = reinterpret_cast<int64_t*>(take(t * 8));
+  const int64_t ntiles = (t + kRadixTile - 1) / kRadixTile;
+  auto* ghist = reinterpret_cast<uint32_t*>(take(256 * ntiles * 4));
+  auto* dtotal = reinterpret_cast<uint32_t*>(take(256 * 4));
+
+  // 1. hash dictionary: unique rows in first-occurrence order, inverse ids
   dict_init_kernel<<<grid_for(cap, 256), 256, 0, stream>>>(keys, rep, cap);
   dict_insert_kernel<<<grid_for(t, 256), 256, 0, stream>>>(rows, t, n, keys, rep,
                                                             static_cast<uint64_t>(cap - 1), inverse_out);
@@ -416,8 +652,29 @@ int tb_unique_rows(const int64_t* rows, int64_t t, int32_t n, int64_t* unique_ou
   tile_sum_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, stream>>>(f, t, bsum);
   scan_bsums_kernel<<<1, kScanThreads, 0, stream>>>(bsum, nb, num_unique);
   tile_scan_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, stream>>>(
-      f, t, bsum, DictSink{rows, n, inverse_out, id_of_slot, unique_out});
+      f, t, bsum, DictSink{rows, n, inverse_out, id_of_slot, uniq_fo});
   dict_finalize_kernel<<<grid_for(t, 256), 256, 0, stream>>>(inverse_out, t, id_of_slot);
+  // 2. lexicographic order of the unique rows (stable LSD radix sort)
+  for (int col = n - 1; col >= 0; --col) {
+    lex_keys_kernel<<<grid_for(t, 256), 256, 0, stream>>>(uniq_fo, n, col, perm_a, col == n - 1, keys_a,
+                                                          num_unique);
+    for (int pass = 0; pass < 8; ++pass) {
+      const int shift = 8 * pass;
+      uint64_t* kin = (pass & 1) ? keys_b : keys_a;
+      uint64_t* kout = (pass & 1) ? keys_a : keys_b;
+      int64_t* pin = (pass & 1) ? perm_b : perm_a;
+      int64_t* pout = (pass & 1) ? perm_a : perm_b;
+      radix_hist_kernel<<<static_cast<unsigned>(ntiles), kRadixThreads, 0, stream>>>(kin, num_unique, shift, ghist,
+                                                                                      ntiles);
+      radix_scan_kernel<<<256, kRadixThreads, 0, stream>>>(ghist, ntiles, num_unique, dtotal);
+      radix_scatter_kernel<<<static_cast<unsigned>(ntiles), kRadixThreads, 0, stream>>>(
+          kin, pin, kout, pout, num_unique, shift, ghist, ntiles, dtotal);
+    }
+  }
+  if (n == 0) lex_keys_kernel<<<grid_for(t, 256), 256, 0, stream>>>(uniq_fo, 1, 0, perm_a, true, keys_a, num_unique);
+  // 3. rows in sorted order, inverse renumbered
+  lex_gather_kernel<<<grid_for(t, 256), 256, 0, stream>>>(uniq_fo, n, perm_a, rank, unique_out, num_unique);
+  lex_inverse_kernel<<<grid_for(t, 256), 256, 0, stream>>>(inverse_out, t, rank);
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }

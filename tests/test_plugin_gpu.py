@@ -18,20 +18,16 @@ pytestmark = pytest.mark.gpu
 
 
 def test_golden_ngram_ops():
+    """unique_rows is byte-identical to the reference's (lexicographic unique
+    rows and their inverse, _kernels.pyx:36-81); the segment kernels too."""
     for op in load_ngram_ops():
         rows = np.array(op["rows"], dtype=np.int64).reshape(-1, op["n"])
         uniq, inv = _backend.unique_rows(rows)
-        # same dictionary as the reference up to a permutation of IDs
-        assert uniq.shape[0] == len(op["unique"])
-        np.testing.assert_array_equal(uniq[inv], rows)
         ref_u = np.array(op["unique"], dtype=np.int64).reshape(-1, op["n"])
         ref_inv = np.array(op["inverse"], dtype=np.int64)
-        # the two ID maps induce the same partition of occurrences
-        perm = {}
-        for a, b in zip(inv.tolist(), ref_inv.tolist()):
-            assert perm.setdefault(a, b) == b
-        np.testing.assert_array_equal(np.sort(uniq.view([("", uniq.dtype)] * op["n"]), axis=0),
-                                      np.sort(ref_u.view([("", ref_u.dtype)] * op["n"]), axis=0))
+        np.testing.assert_array_equal(uniq, ref_u)
+        np.testing.assert_array_equal(inv, ref_inv)
+        np.testing.assert_array_equal(uniq[inv], rows)
         seg = np.array(op["seg"], dtype=np.int64)
         flat = np.array(op["flat"], dtype=np.int64)
         counts = _backend.segment_bincount(flat, seg, op["u"])
@@ -40,18 +36,35 @@ def test_golden_ngram_ops():
         np.testing.assert_array_equal(_backend.clipped_numerators(flat, seg, rm), op["clipped"])
 
 
-def test_unique_rows_first_occurrence_order_and_large():
-    rng = np.random.default_rng(0)
-    rows = rng.integers(0, 30, size=(200_000, 3))
+@pytest.mark.parametrize("n,hi", [(1, 1 << 40), (3, 30), (4, 128000), (2, 1 << 62)])
+def test_unique_rows_lexicographic_like_numpy_large(n, hi):
+    """np.unique(axis=0) is the reference python backend's order
+    (_py_kernels.py:24-33: lexsort over the columns, signed int64)."""
+    rng = np.random.default_rng(n)
+    rows = rng.integers(-hi, hi, size=(200_000, n))
+    rows[100_000:150_000] = rows[:50_000]  # duplicates
     uniq, inv = _backend.unique_rows(rows)
-    np.testing.assert_array_equal(uniq[inv], rows)
-    assert uniq.shape[0] == np.unique(rows, axis=0).shape[0]
-    # IDs appear in first-occurrence order
-    first = np.unique(inv, return_index=True)[1]
-    assert np.all(np.diff(first) > 0)
+    ref_u, ref_inv = np.unique(rows, axis=0, return_inverse=True)
+    np.testing.assert_array_equal(uniq, ref_u)
+    np.testing.assert_array_equal(inv, ref_inv.reshape(-1))
     d_uniq, d_inv = _backend.unique_rows(torch.as_tensor(rows, device="cuda"))
     assert d_uniq.is_cuda
     np.testing.assert_array_equal(d_inv.cpu().numpy(), inv)
+    np.testing.assert_array_equal(d_uniq.cpu().numpy(), uniq)
+
+
+def test_unique_rows_matches_reference_backend():
+    bb = oracle.reference_package()
+    if bb is None:
+        pytest.skip("reference package not built")
+    from batchbleu import _py_kernels
+    rng = np.random.default_rng(5)
+    for t, n, v in [(1, 1, 5), (17, 2, 3), (5000, 4, 50), (3000, 1, 2)]:
+        rows = rng.integers(0, v, size=(t, n))
+        ru, ri = _py_kernels.unique_rows(rows)
+        u, i = _backend.unique_rows(rows)
+        np.testing.assert_array_equal(u, ru)
+        np.testing.assert_array_equal(i, ri)
 
 
 def test_unique_rows_empty():
@@ -250,3 +263,26 @@ def test_batched_matches_oracle_property(case):
                                       smoothing=sm) for i in range(len(clen))]
     np.testing.assert_allclose(got, serial, atol=1e-12)
     assert np.all(got >= 0.0) and np.all(got <= 1.0)
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int64])
+def test_flatten_windows_kernel_matches_reference_layout(dtype):
+    """tb_flatten_windows (flatten_valid on CUDA slices) == the reference's
+    numpy flatten_valid (ngrams.py:79-83): same rows, same row-major order,
+    ragged lengths, rows shorter than n, empty rows, strided row views."""
+    rng = np.random.default_rng(11)
+    for b, l, n in [(1, 1, 1), (7, 5, 3), (64, 40, 4), (300, 129, 2), (5, 3, 4)]:
+        ids = rng.integers(0, 1 << 30, size=(b, l))
+        lens = rng.integers(0, l + 1, size=b)
+        want = flatten_valid(tb.extract_ngrams(tb.TokenBatch(ids=ids, lengths=lens), n))
+        dev = tb.TokenBatch(ids=torch.as_tensor(ids, device="cuda", dtype=dtype),
+                            lengths=torch.as_tensor(lens, device="cuda"))
+        got = flatten_valid(tb.extract_ngrams(dev, n))
+        assert got.is_cuda and got.dtype == torch.int64
+        np.testing.assert_array_equal(got.cpu().numpy(), want)
+    wide = torch.as_tensor(rng.integers(0, 99, size=(6, 50)), device="cuda", dtype=dtype)
+    view = tb.TokenBatch.trusted(wide[:, :20], torch.full((6,), 17, device="cuda"))
+    got = flatten_valid(tb.extract_ngrams(view, 3)).cpu().numpy()
+    host = wide[:, :20].cpu().numpy()
+    np.testing.assert_array_equal(got, np.concatenate([np.lib.stride_tricks.sliding_window_view(r[:17], 3)
+                                                       for r in host]))
