@@ -57,7 +57,12 @@ extern "C" {
 #define TB_SMOOTH_ADD_K 2
 #define TB_SMOOTH_EXP 3
 
-/* Limits of the device path: both are kernel-parameter array sizes. */
+/* Limits of the FUSED kernels (tb_bleu_stats / tb_bleu_host / tb_bleu_scores):
+ * kernel-parameter array sizes.  Larger N or R are served by the n-gram
+ * operator kernels below (tb_flatten_windows, tb_unique_rows,
+ * tb_segment_bincount, tb_count_binary, tb_clipped_numerators) and
+ * tb_bleu_scores_any / tb_bleu_totals, composed by the Python host
+ * (paper_2510_05485_b200.bleu), so the public API has no limit. */
 #define TB_MAX_ORDER 32
 #define TB_MAX_REFS 32
 
@@ -175,8 +180,20 @@ int tb_bleu_scores(const int64_t* num, const int64_t* den,
                    double* scores_out, double* precisions_out, double* bp_out,
                    void* stream);
 
+/* tb_bleu_scores for ANY max_order (the reference caps neither N nor R;
+ * bleu.py:24-56), with the normalised weights in DEVICE memory (N,) fp64.
+ * fp32 = 0: fp64 in numpy's operation order (outputs double*); fp32 = 1: the
+ * same operations in single precision, outputs float* (north_star: within
+ * 1e-5 relative of the fp64 scores).  Any output may be NULL. */
+int tb_bleu_scores_any(const int64_t* num, const int64_t* den,
+                       const int64_t* cand_len, const int64_t* eff_ref,
+                       int64_t batch, int32_t max_order,
+                       int32_t smoothing, double eps, double k, const double* weights_dev,
+                       int32_t fp32, void* scores_out, void* precisions_out, void* bp_out,
+                       void* stream);
+
 /* Corpus aggregation `score_corpus_from_stats` (bleu.py:295-300): column sums
- * of (B, N) num/den and (B,) lengths into totals (2N+2,) int64. */
+ * of (B, N) num/den and (B,) lengths into totals (2N+2,) int64 (any N). */
 int tb_bleu_totals(const int64_t* num, const int64_t* den,
                    const int64_t* cand_len, const int64_t* eff_ref,
                    int64_t batch, int32_t max_order, int64_t* totals_out,

@@ -74,6 +74,8 @@ SIGNATURES = {
     "tb_bleu_scores": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _F64, _F64, _P,
                                       _P, _P, _P, _P]),
     "tb_bleu_totals": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _P]),
+    "tb_bleu_scores_any": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _F64, _F64, _P, _I32,
+                                          _P, _P, _P, _P]),
     "tb_validate_batch": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64, _P, _P]),
     "tb_validate_host": (ctypes.c_int, [_I32, _P, _I64, _I64, _P, _I64]),
     "tb_windows_workspace_bytes": (_SZ, [_I64]),

@@ -110,9 +110,6 @@ def _check_batches(candidates: TokenBatch, references: Sequence[TokenBatch]) -> 
             raise ValueError(
                 f"reference batch size {ref.batch_size} does not match "
                 f"candidate batch size {candidates.batch_size}")
-    if len(references) > _native.TB_MAX_REFS:
-        raise ValueError(f"at most {_native.TB_MAX_REFS} reference sets are supported, "
-                         f"got {len(references)}")
 
 
 # ---------------------------------------------------------------------------
@@ -246,8 +243,8 @@ def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: Bl
 
     Returns (host_mode, tensors dict on device, device-side output buffer)."""
     _check_batches(candidates, references)
-    if config.max_order > _native.TB_MAX_ORDER:
-        raise ValueError(f"max_order > {_native.TB_MAX_ORDER} is not supported by the device path")
+    if config.max_order > _native.TB_MAX_ORDER or len(references) > _native.TB_MAX_REFS:
+        return _launch_unbounded(candidates, references, config, mode)
     if not candidates.is_device:
         return _launch_host(candidates, references, config, mode)
     device = candidates.ids.device
@@ -311,6 +308,48 @@ def _launch(candidates: TokenBatch, references: Sequence[TokenBatch], config: Bl
         _native.check(rc, "tb_bleu_stats")
 
     return False, views, None
+
+
+def _launch_unbounded(candidates: TokenBatch, references: Sequence[TokenBatch], config: BleuConfig,
+                      mode: str):
+    """More reference sets or orders than the fused kernels take: the
+    reference's per-order algorithm on the device n-gram operator kernels
+    (unbounded.py).  Same outputs and result types as _launch."""
+    from . import unbounded
+    host = not candidates.is_device
+    dev = candidates.ids.device if not host else _native.require_cuda()
+    with torch.cuda.device(dev):
+        num, den, cl, er = unbounded.stats(candidates, references, config.max_order, dev)
+        if mode == "stats":
+            out = {"num": num, "den": den, "cand_len": cl, "eff_ref": er}
+        elif mode == "sentence":
+            sc, prec, bp = unbounded.scores(num, den, cl, er, config, dev)
+            out = {"scores": sc, "precisions": prec, "bp": bp}
+        else:
+            N = config.max_order
+            tot = unbounded.totals(num, den, cl, er, dev)
+            sc, prec, bp = unbounded.scores(tot[None, :N], tot[None, N:2 * N].contiguous(), tot[2 * N:2 * N + 1],
+                                            tot[2 * N + 1:2 * N + 2], config, dev)
+            out = {"totals": tot, "corpus": torch.cat([sc, bp, prec[0]])}
+    if host:
+        out = {k: v.cpu().numpy() for k, v in out.items()}
+    return host, out, None
+
+
+def check_device_flags(device=None) -> None:
+    """Synchronise with `device` (default: the current CUDA device) and raise
+    ValueError if a device-resident call since the last check met bad input
+    data — lengths outside [0, width] in batches built with
+    TokenBatch.trusted (the kernels clamp them and OR a flag instead of
+    stopping); the flag word is cleared.  Device calls never synchronise on
+    their own, so this is how an asynchronous training loop surfaces them."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    err = _err_words.get(dev.index)
+    if err is None:
+        return
+    flags = int(err.item())
+    err.zero_()
+    _native.raise_flags(flags)
 
 
 def compute_stats(candidates: TokenBatch, references: Sequence[TokenBatch],
@@ -379,12 +418,19 @@ def _stats_on_device(stats: SentenceStats):
     return True, dev, out
 
 
-def _epilogue(stats: SentenceStats, config: BleuConfig, want_scores: bool):
+def _epilogue(stats: SentenceStats, config: BleuConfig, want_scores: bool, fp32: bool = False):
     lib = _native.load()
     host, dev, (num, den, cl, er) = _stats_on_device(stats)
     if num.dim() != 2 or num.shape[1] != config.max_order:
         raise ValueError(f"numerators must be (B, {config.max_order})")
     B, N = num.shape
+    if fp32 or N > _native.TB_MAX_ORDER:  # any N / the fp32 epilogue: tb_bleu_scores_any
+        from . import unbounded
+        with torch.cuda.device(dev):
+            sc, prec, bp = unbounded.scores(num.contiguous(), den.contiguous(), cl, er, config, dev, fp32=fp32)
+        if host:
+            return (sc.cpu().numpy() if want_scores else None), prec.cpu().numpy(), bp.cpu().numpy()
+        return (sc if want_scores else None), prec, bp
     with torch.cuda.device(dev):
         prec = torch.empty((B, N), dtype=torch.float64, device=dev)
         bp = torch.empty(B, dtype=torch.float64, device=dev)
@@ -405,9 +451,13 @@ def apply_smoothing(stats: SentenceStats, config: BleuConfig):
     return _epilogue(stats, config, want_scores=False)[1]
 
 
-def score_sentences_from_stats(stats: SentenceStats, config: BleuConfig) -> BleuResult:
-    """bleu.py:274-279."""
-    sc, prec, bp = _epilogue(stats, config, want_scores=True)
+def score_sentences_from_stats(stats: SentenceStats, config: BleuConfig, *,
+                               dtype=None) -> BleuResult:
+    """bleu.py:274-279.  dtype=torch.float32 (or np.float32) runs the fp32
+    epilogue (north_star: within 1e-5 relative of fp64); default fp64 in
+    numpy's operation order."""
+    fp32 = dtype in (torch.float32, np.float32)
+    sc, prec, bp = _epilogue(stats, config, want_scores=True, fp32=fp32)
     return BleuResult(scores=sc, precisions=prec, brevity_penalty=bp)
 
 

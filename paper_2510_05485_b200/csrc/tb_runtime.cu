@@ -35,6 +35,70 @@ __global__ void bleu_scores_kernel(const int64_t* __restrict__ num, const int64_
   }
 }
 
+// Any max_order, weights in device memory; R = double (fp64, numpy's
+// operation order as bleu_epilogue: explicit round-to-nearest operations, no
+// FMA contraction) or float (the fp32 epilogue: the same operations in single
+// precision, outputs float).  One thread per sentence.
+__device__ __forceinline__ double r_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double r_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double r_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double r_div(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double r_log(double a) { return log(a); }
+__device__ __forceinline__ double r_exp(double a) { return exp(a); }
+__device__ __forceinline__ float r_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float r_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float r_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float r_div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float r_log(float a) { return logf(a); }
+__device__ __forceinline__ float r_exp(float a) { return expf(a); }
+
+template <typename R>
+__global__ void bleu_scores_any_kernel(const int64_t* __restrict__ num, const int64_t* __restrict__ den,
+                                       const int64_t* __restrict__ cand_len, const int64_t* __restrict__ eff_ref,
+                                       int64_t batch, int N, int smoothing, double eps, double kk,
+                                       const double* __restrict__ w, R* scores, R* precisions, R* bp_out) {
+  const R eps_r = static_cast<R>(eps), k_r = static_cast<R>(kk);
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < batch;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // _bp_vector, bleu.py:256-261: 0 for an empty candidate, 1 if c > r, else exp(1 - r/c)
+    const R cd = static_cast<R>(cand_len[b]);
+    const R rd = static_cast<R>(eff_ref[b]);
+    R bp = cd > rd ? R(1) : r_exp(r_sub(R(1), r_div(rd, cd > R(0) ? cd : R(1))));
+    if (!(cd > R(0))) bp = R(0);
+    R counter = 1, s = 0;
+    bool ok = true;
+    for (int n = 0; n < N; ++n) {
+      const int64_t nn = num[b * N + n], dn = den[b * N + n];
+      const R nd = static_cast<R>(nn), dd = static_cast<R>(dn);
+      const bool has_den = dn > 0;
+      R pn = (has_den && nn != 0) ? r_div(nd, dd) : R(0);      // bleu.py:222
+      const bool zero_num = has_den && nn == 0;                 // bleu.py:223
+      if (smoothing == TB_SMOOTH_FLOOR) {
+        if (zero_num) pn = r_div(eps_r, dd);                    // bleu.py:228
+      } else if (smoothing == TB_SMOOTH_ADD_K) {
+        if (n >= 1 && has_den) pn = r_div(r_add(nd, k_r), r_add(dd, k_r));  // bleu.py:230-232
+      } else if (smoothing == TB_SMOOTH_EXP) {
+        if (zero_num) {                                         // bleu.py:234-238, exact 2^counter
+          pn = r_div(R(1), r_mul(static_cast<R>(ldexp(1.0, static_cast<int>(counter))), dd));
+          counter = r_add(counter, R(1));
+        }
+      }
+      if (precisions) precisions[b * N + n] = pn;
+      const R wn = static_cast<R>(w[n]);
+      if (wn > R(0)) {                                          // bleu.py:242-253, sequential sum
+        if (pn > R(0))
+          s = r_add(s, r_mul(r_log(pn), wn));
+        else
+          ok = false;
+      }
+    }
+    R score = ok ? r_mul(bp, r_exp(s)) : R(0);
+    score = score < R(0) ? R(0) : (score > R(1) ? R(1) : score);
+    if (bp_out) bp_out[b] = bp;
+    if (scores) scores[b] = score;
+  }
+}
+
 // one CTA per output column: [num_0..N-1 | den_0..N-1 | cand_len | eff_ref]
 __global__ void bleu_totals_kernel(const int64_t* __restrict__ num, const int64_t* __restrict__ den,
                                    const int64_t* __restrict__ cand_len,
@@ -1199,12 +1263,37 @@ int tb_bleu_totals(const int64_t* num, const int64_t* den, const int64_t* cand_l
                    const int64_t* eff_ref, int64_t batch, int32_t max_order, int64_t* totals_out,
                    void* stream) {
   StreamDeviceGuard device_guard(stream);
-  if (max_order < 1) return TB_ERR_INVALID_ARG;
-  if (max_order > TB_MAX_ORDER) return TB_ERR_UNSUPPORTED;
+  if (max_order < 1) return TB_ERR_INVALID_ARG;  // any order: one CTA per output column
   if (batch < 0 || !totals_out) return TB_ERR_INVALID_ARG;
   if (batch > 0 && (!num || !den || !cand_len || !eff_ref)) return TB_ERR_INVALID_ARG;
   bleu_totals_kernel<<<2 * max_order + 2, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       num, den, cand_len, eff_ref, batch, max_order, totals_out);
+  TB_CUDA(cudaGetLastError());
+  return TB_OK;
+}
+
+int tb_bleu_scores_any(const int64_t* num, const int64_t* den, const int64_t* cand_len, const int64_t* eff_ref,
+                       int64_t batch, int32_t max_order, int32_t smoothing, double eps, double k,
+                       const double* weights_dev, int32_t fp32, void* scores_out, void* precisions_out, void* bp_out,
+                       void* stream) {
+  StreamDeviceGuard device_guard(stream);
+  if (max_order < 1 || smoothing < TB_SMOOTH_NONE || smoothing > TB_SMOOTH_EXP || !(eps > 0) || !(k > 0))
+    return TB_ERR_INVALID_ARG;
+  if (batch < 0) return TB_ERR_INVALID_ARG;
+  if (batch == 0) return TB_OK;
+  if (!num || !den || !cand_len || !eff_ref || !weights_dev) return TB_ERR_INVALID_ARG;
+  const int threads = 128;
+  int64_t blocks = (batch + threads - 1) / threads;
+  if (blocks > 65535) blocks = 65535;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (fp32)
+    bleu_scores_any_kernel<float><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
+        num, den, cand_len, eff_ref, batch, max_order, smoothing, eps, k, weights_dev,
+        static_cast<float*>(scores_out), static_cast<float*>(precisions_out), static_cast<float*>(bp_out));
+  else
+    bleu_scores_any_kernel<double><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
+        num, den, cand_len, eff_ref, batch, max_order, smoothing, eps, k, weights_dev,
+        static_cast<double*>(scores_out), static_cast<double*>(precisions_out), static_cast<double*>(bp_out));
   TB_CUDA(cudaGetLastError());
   return TB_OK;
 }

@@ -36,6 +36,9 @@ class SentenceBleuPlan:
                  sentence: bool = True):
         config = config or BleuConfig()
         _check_batches(candidates, references)
+        if len(references) > _native.TB_MAX_REFS or config.max_order > _native.TB_MAX_ORDER:
+            raise ValueError(f"SentenceBleuPlan binds the fused kernel: at most {_native.TB_MAX_REFS} reference "
+                             f"sets and max_order {_native.TB_MAX_ORDER} (sentence_bleu takes any)")
         if not candidates.is_device or not all(r.is_device for r in references):
             raise ValueError("SentenceBleuPlan needs TokenBatch objects holding CUDA tensors")
         lib = _native.load()

@@ -187,9 +187,6 @@ def test_max_refs_and_long_orders():
     rng = np.random.default_rng(9)
     (cid, clen), refs = _correlated(rng, 8, 64, 6, 32)
     _check_against_oracle(cid, clen, refs, tb.BleuConfig(max_order=8, smoothing="exp"))
-    with pytest.raises(ValueError):
-        cand, rb = _batches(cid, clen, refs + refs[:1], "cuda")
-        tb.sentence_bleu(cand, rb)
 
 
 @pytest.mark.parametrize("order", [5, 9, 13])
@@ -414,9 +411,14 @@ def test_kernel_flags_bad_lengths_for_trusted_batches():
     ids = torch.zeros((2, 3), dtype=torch.int64, device="cuda")
     bad = tb.TokenBatch.trusted(ids, torch.tensor([1, 4], device="cuda"))
     ok = tb.TokenBatch(ids=np.zeros((2, 3), dtype=np.int64), lengths=[1, 1])
-    # device mode does not synchronise; the host-mode launch reports the flag
+    # device mode does not synchronise: check_device_flags surfaces (and clears) the flag
+    tb.check_device_flags()
     res = tb.sentence_bleu(bad, [bad])
     assert res.scores.shape == (2,)
+    with pytest.raises(ValueError, match="lengths"):
+        tb.check_device_flags()
+    tb.check_device_flags()  # cleared
+    # the host-mode launch reports it at once
     with pytest.raises(ValueError):
         tb.sentence_bleu(ok, [tb.TokenBatch.trusted(ids, torch.tensor([1, 4], device="cuda"))])
 
