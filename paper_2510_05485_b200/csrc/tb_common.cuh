@@ -496,16 +496,15 @@ __device__ void finalize_launch(const StatsParams& p, unsigned long long* s_tot)
   const int N = p.max_order;
   const int nt = 2 * N + 2;
   const bool corpus = p.totals != nullptr || p.corpus != nullptr;
-  if (corpus) {
-    for (int j = tid; j < nt; j += blockDim.x) s_tot[j] = 0;
-    __syncthreads();
-    for (int i = tid; i < kAccCopies * nt; i += blockDim.x) {
-      const unsigned long long v = atomicExch(&p.acc[i], 0ull);
-      if (v) atomicAdd(&s_tot[i % nt], v);
+  if (corpus) {  // thread j sums slot j over the copies (measured faster than
+    // spreading the copies over the CTA with shared atomics: c4 40.4 vs 41.7 us)
+    for (int j = tid; j < nt; j += blockDim.x) {
+      unsigned long long sum = 0;
+      for (int c = 0; c < kAccCopies; ++c) sum += atomicExch(&p.acc[c * nt + j], 0ull);
+      s_tot[j] = sum;
+      if (p.totals) p.totals[j] = static_cast<int64_t>(sum);
     }
     __syncthreads();
-    for (int j = tid; j < nt; j += blockDim.x)
-      if (p.totals) p.totals[j] = static_cast<int64_t>(s_tot[j]);
   }
   if (tid == 0) {
     const int f = atomicExch(p.ws_flag, 0);
@@ -538,19 +537,19 @@ __device__ __forceinline__ bool arrive_last(const StatsParams& p, unsigned int p
 // End of a CTA of the CTA-per-group kernels.  nb (list mode): the number of
 // listed groups; only the CTAs that got one take part (none when nothing was
 // listed: the warp-group kernel has finished the launch).
+template <bool listed = false>
 __device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int& s_flags, int& s_last,
                            int64_t nb = -1) {
   const int tid = threadIdx.x;
   const int N = p.max_order;
   const bool corpus = p.totals != nullptr || p.corpus != nullptr;
-  const bool listed = p.glist != nullptr;
   if (!corpus && !p.err_store && !listed) {  // no cross-CTA work: report flags directly (the caller zeroed *err)
     __syncthreads();
     if (tid == 0 && s_flags) atomicOr(p.err, s_flags);
     return;
   }
   unsigned int participants = gridDim.x;
-  if (listed) {
+  if constexpr (listed) {
     if (nb < 1) return;
     participants = static_cast<unsigned int>(nb < gridDim.x ? nb : gridDim.x);
     if (blockIdx.x >= participants) return;  // no group, no flags, no totals
@@ -564,6 +563,7 @@ __device__ void finish_cta(const StatsParams& p, unsigned long long* s_tot, int&
   __syncthreads();
   if (s_last) finalize_launch(p, s_tot);
 }
+
 
 
 // Debug-only phase timestamps (build with -DTB_PHASES; see tools/phase_profile.py)

@@ -21,7 +21,7 @@ namespace {
 // rc[r][o]: occurrences in reference r of the key owned by candidate position o.
 // --------------------------------------------------------------------------
 
-template <typename T>
+template <typename T, bool kList>
 __global__ void __launch_bounds__(kMultiThreads, 2)
     bleu_multi_kernel(const __grid_constant__ StatsParams p) {
   constexpr int NT = kMultiThreads;
@@ -77,8 +77,8 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
   }
   griddep_wait_and_release();
   // list mode: the dense groups listed by the warp-per-group kernel before this one
-  const int64_t nb = p.glist ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned int*>(p.gcount)) : p.batch;
-  auto group_at = [&](int64_t i) -> int64_t { return p.glist ? static_cast<int64_t>(p.glist[i]) : i; };
+  const int64_t nb = kList ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned int*>(p.gcount)) : p.batch;
+  auto group_at = [&](int64_t i) -> int64_t { return kList ? static_cast<int64_t>(p.glist[i]) : i; };
   if (static_cast<int64_t>(blockIdx.x) < nb) issue_stage(group_at(blockIdx.x));
   __syncthreads();
   TB_MARK(0);
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
     }
     TB_MARK(30);
   }
-  finish_cta(p, s_tot, s_flags, s_last, nb);
+  finish_cta<kList>(p, s_tot, s_flags, s_last, nb);
   TB_MARK(31);
 }
 
@@ -647,10 +647,13 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
 namespace tbk {
 
 int launch_multi(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes) {
-  static size_t attr_set[2][64] = {};
+  static size_t attr_set[4][64] = {};
+  const bool list = prm.glist != nullptr;
   if (token_bytes == 4)
-    return launch_kernel(bleu_multi_kernel<int32_t>, prm, pl, sms, true, attr_set[0], stream, kMultiThreads);
-  return launch_kernel(bleu_multi_kernel<int64_t>, prm, pl, sms, true, attr_set[1], stream, kMultiThreads);
+    return list ? launch_kernel(bleu_multi_kernel<int32_t, true>, prm, pl, sms, true, attr_set[2], stream, kMultiThreads)
+                : launch_kernel(bleu_multi_kernel<int32_t, false>, prm, pl, sms, true, attr_set[0], stream, kMultiThreads);
+  return list ? launch_kernel(bleu_multi_kernel<int64_t, true>, prm, pl, sms, true, attr_set[3], stream, kMultiThreads)
+              : launch_kernel(bleu_multi_kernel<int64_t, false>, prm, pl, sms, true, attr_set[1], stream, kMultiThreads);
 }
 
 #ifdef TB_PHASES

@@ -18,9 +18,13 @@ namespace {
 //   verify: the winner owns the slot (its own occurrence is counted
 //           implicitly); an equal token adds one to the owner's count word
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 4)
+// NT threads per CTA: 256 (4 CTAs per SM) for batches of many groups, 512
+// (2 per SM) when the batch is one wave: every phase then has half the work per
+// thread, which is the per-group latency the step waits for.
+template <typename T, int NT, bool kList>
+__global__ void __launch_bounds__(NT, 1024 / NT)
     bleu_pair_kernel(const __grid_constant__ StatsParams p) {
+  constexpr int kThreads = NT;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned int s_hits[TB_MAX_ORDER];
   __shared__ int64_t s_len[2];
@@ -72,15 +76,16 @@ __global__ void __launch_bounds__(kThreads, 4)
   }
   griddep_wait_and_release();
   // list mode: the dense groups listed by the warp-per-group kernel before this one
-  const int64_t nb = p.glist ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned int*>(p.gcount)) : p.batch;
-  auto group_at = [&](int64_t i) -> int64_t { return p.glist ? static_cast<int64_t>(p.glist[i]) : i; };
+  // (a template parameter: the runtime test cost the batch path 0.6 us at c4)
+  const int64_t nb = kList ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned int*>(p.gcount)) : p.batch;
+  auto group_at = [&](int64_t i) -> int64_t { return kList ? static_cast<int64_t>(p.glist[i]) : i; };
   if (static_cast<int64_t>(blockIdx.x) < nb) issue_stage(group_at(blockIdx.x), 0);
   __syncthreads();
   TB_MARK(0);
   uint32_t phases = 0;  // bit i: parity of mbarrier i
   // off after a group of this CTA needed the hash passes (related text); listed
   // groups are known to need them
-  bool try_filter = p.glist == nullptr;
+  bool try_filter = !kList;
 
   for (int64_t gi = blockIdx.x; gi < nb; gi += gridDim.x) {
     const int64_t b = group_at(gi);
@@ -211,10 +216,14 @@ __global__ void __launch_bounds__(kThreads, 4)
         // marks the matched ones)
         *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
         *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
+        // (an early exit once more survivors than the exact match takes were
+        // listed — related text — saved 1.8 us at c2 related but cost 0.5 us
+        // at c2 uniform: the loop stays branch-free)
         for (; pm; pm &= pm - 1) {
           const int j = atomicAdd(&s_nf, 1);
           if (j < kSmallSet) s_flist[j] = static_cast<uint16_t>(p0 + __ffs(pm) - 1);
         }
+
       }
       __syncthreads();
       TB_MARK(21);
@@ -405,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         warp_append_quad(lx + roff, &s_nr, fm, [&](int k) { return p0 + k; }, lane);
       }
       if (__syncthreads_or(left))
-        pair_resolve_lost(own, cnt, lost, nl, id1, mask, hshift, roff, tid, hash1, eq1, 2);
+        pair_resolve_lost<NT>(own, cnt, lost, nl, id1, mask, hshift, roff, tid, hash1, eq1, 2);
       TB_MARK(3);
       const int nd = s_ndef;
       for (int i0 = 0; i0 < nd; i0 += kThreads) {  // deferred lookups: the full chain
@@ -604,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         }
       }
       __syncthreads();
-      if (s_nlost) list_resolve_lost(own, cnt, kc, lout, s_nlost, lin, idn, mask, hshift, tid);
+      if (s_nlost) list_resolve_lost<NT>(own, cnt, kc, lout, s_nlost, lin, idn, mask, hshift, tid);
       if (s_ndef) {
         const int nd = s_ndef;
         for (int j = tid; j < nd; j += kThreads) {
@@ -738,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     }
     TB_MARK(30);
   }
-  finish_cta(p, s_tot, s_flags, s_last, nb);
+  finish_cta<kList>(p, s_tot, s_flags, s_last, nb);
   TB_MARK(31);
 }
 
@@ -747,10 +756,15 @@ __global__ void __launch_bounds__(kThreads, 4)
 namespace tbk {
 
 int launch_pair(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes) {
-  static size_t attr_set[2][64] = {};
+  static size_t attr_set[4][64] = {};
+  // (512-thread CTAs, bleu_pair_kernel<T, 512, .>, measured no faster on single
+  // waves of few groups: c1 5.48 vs 5.60 us; 256 everywhere)
+  const bool list = prm.glist != nullptr;  // the groups listed by the filter kernel
   if (token_bytes == 4)
-    return launch_kernel(bleu_pair_kernel<int32_t>, prm, pl, sms, true, attr_set[0], stream);
-  return launch_kernel(bleu_pair_kernel<int64_t>, prm, pl, sms, true, attr_set[1], stream);
+    return list ? launch_kernel(bleu_pair_kernel<int32_t, 256, true>, prm, pl, sms, true, attr_set[2], stream)
+                : launch_kernel(bleu_pair_kernel<int32_t, 256, false>, prm, pl, sms, true, attr_set[0], stream);
+  return list ? launch_kernel(bleu_pair_kernel<int64_t, 256, true>, prm, pl, sms, true, attr_set[3], stream)
+              : launch_kernel(bleu_pair_kernel<int64_t, 256, false>, prm, pl, sms, true, attr_set[1], stream);
 }
 
 #ifdef TB_PHASES

@@ -46,8 +46,9 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
                                    static_cast<int>(pl.smem_bytes)));
     // one shared-memory carveout for every stats kernel (no reconfiguration
     // between back-to-back launches of different kernels)
-    TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared));
+    if (!getenv("TB_DEBUG_NO_CARVEOUT"))
+      TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
     attr_set[dev & 63] = pl.smem_bytes + 1;
   }
   int64_t grid = pl.grid;

@@ -31,13 +31,24 @@ NAMES[23] = "epi.math"
 NAMES.update({20: "f.bitmaps", 21: "f.filter", 22: "f.match"})
 
 
+def build():
+    import subprocess
+    sys.path.insert(0, ROOT)
+    import __graft_entry__ as g
+    out = os.path.join(_native.PKG_DIR, "libtensorbleu_b200_phases.so")
+    subprocess.check_call([g._nvcc(), *g.NVCC_FLAGS, "-DTB_PHASES", *g.SOURCES, "-o", out], cwd=g.CSRC)
+
+
 def main():
+    if "--build" in sys.argv:
+        build()
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--dtype", default="int32")
     ap.add_argument("--data", default="uniform")
     args = ap.parse_args()
-    b, l, v, r, sm = bench.WORKLOADS[args.workload]
+    b, l, v, r, sm = bench.WORKLOADS[args.workload][:5]
     (cid, clen), refs = bench.generate_batch(b, l, v, r, data=args.data)
     dt = torch.int32 if args.dtype == "int32" else torch.int64
     cand = tb.TokenBatch(ids=torch.as_tensor(cid).cuda().to(dt), lengths=torch.as_tensor(clen).cuda())
