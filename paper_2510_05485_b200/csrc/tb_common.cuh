@@ -168,6 +168,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -678,6 +685,31 @@ __device__ __forceinline__ uint32_t pair_insert_loser(uint16_t* own, uint32_t* c
   }
 }
 
+// Barriers of a thread subset: BAR == 0 is the whole CTA (__syncthreads);
+// otherwise named barrier BAR over the NT threads that take part.
+template <int NT, int BAR>
+__device__ __forceinline__ void bsync() {
+  if constexpr (BAR == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+}
+template <int NT, int BAR>
+__device__ __forceinline__ int bsync_or(int v) {
+  if constexpr (BAR == 0) {
+    return __syncthreads_or(v);
+  } else {
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %1, 0;\n\t"
+        "bar.red.or.pred p, %2, %3, p;\n\tselp.s32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"(v), "n"(BAR), "n"(NT)
+        : "memory");
+    return r;
+  }
+}
+
 // Round-r slot of a key whose round-1 home is the top bits of h (r >= 1):
 // independent multiplicative remixes of the same 32-bit hash.
 __device__ __forceinline__ uint32_t rehash(uint32_t h, int r, uint32_t hshift) {
@@ -710,7 +742,7 @@ __device__ __forceinline__ void pair_retry_store(uint16_t* own, uint32_t h, int 
 // done the store half of round 1 (in its home-slot verify pass) and a barrier
 // (with first_round > 1, rounds before it are complete and the store half of
 // first_round is done).  `ids[pos]` receives the final slot.  All threads call it.
-template <int NT = kThreads, typename HashF, typename EqF>
+template <int NT = kThreads, int BAR = 0, typename HashF, typename EqF>
 __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, uint16_t* lost, int nl, uint16_t* ids,
                                                   uint32_t mask, uint32_t hshift, int roff, int tid, HashF hash,
                                                   EqF eq, int first_round = 1) {
@@ -731,7 +763,7 @@ __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, 
         if (r < kRetryRounds) pair_retry_store(own, h, r + 1, hshift, pos);
       }
     }
-    if (!__syncthreads_or(left)) return;
+    if (!bsync_or<NT, BAR>(left)) return;
   }
   for (int i = tid; i < nl; i += NT) {
     const uint16_t pos = lost[i];
@@ -739,13 +771,13 @@ __device__ __forceinline__ void pair_resolve_lost(uint16_t* own, uint32_t* cnt, 
     ids[pos] = static_cast<uint16_t>(pair_insert_loser(own, cnt, ids[pos], mask, pos, pos < roff ? 1u : (1u << 16),
                                                        [&](uint16_t x) { return eq(pos, x); }));
   }
-  __syncthreads();
+  bsync<NT, BAR>();
 }
 
 // pair_resolve_lost for the live-list passes of orders >= 2: `lost` holds list
 // indices e (owners are list indices, keys kc[e], hash key * 0x9E3779B1), all of
 // candidate entries; settling e writes its owner's list index to idn[lin[e]].
-template <int NT = kThreads>
+template <int NT = kThreads, int BAR = 0>
 __device__ __forceinline__ void list_resolve_lost(uint16_t* own, uint32_t* cnt, const uint32_t* kc, uint16_t* lost,
                                                   int nl, const uint16_t* lin, uint16_t* idn, uint32_t mask,
                                                   uint32_t hshift, int tid) {
@@ -766,7 +798,7 @@ __device__ __forceinline__ void list_resolve_lost(uint16_t* own, uint32_t* cnt, 
         if (r < kRetryRounds) pair_retry_store(own, h, r + 1, hshift, e);
       }
     }
-    if (!__syncthreads_or(left)) return;
+    if (!bsync_or<NT, BAR>(left)) return;
   }
   for (int i = tid; i < nl; i += NT) {
     const uint16_t e = lost[i];
@@ -778,7 +810,7 @@ __device__ __forceinline__ void list_resolve_lost(uint16_t* own, uint32_t* cnt, 
     asm volatile("ld.volatile.shared.u16 %0, [%1];" : "=h"(w) : "r"(smem_u32(own) + 2 * sl));
     idn[lin[e]] = w;
   }
-  __syncthreads();
+  bsync<NT, BAR>();
 }
 
 // Warp-aggregated appends to a shared list (one atomic per warp).  All 32 lanes
@@ -843,5 +875,267 @@ __device__ __forceinline__ int pair_find_retry(const uint16_t* own, const T* tok
   }
 }
 
+
+// --------------------------------------------------------------------------
+// Exact clipped counts of a short element list (the filter kernel's listed
+// survivors, the pair kernel's finisher warp): elements sorted by (row,
+// position), counted per order with match.any (S <= 32) or a tiny hash table
+// per order (S <= kSparseMax).
+// --------------------------------------------------------------------------
+constexpr int kSparseMax = 128;  // listed elements handled per group
+constexpr int kTinySlots = 256;  // tiny table (>= 2 * kSparseMax)
+
+// Element list key: (row << 23) | (position << 7) | list slot — sorting keys
+// sorts by (row, position) and carries the slot of the element's token.
+__device__ __forceinline__ uint32_t elem_key(uint32_t side, uint32_t pos, uint32_t slot) {
+  return (side << 23) | (pos << 7) | slot;
+}
+
+// Bitonic sort (ascending) of 32 * K keys in a warp; element i = j * 32 + lane is key[j].
+template <int K>
+__device__ __forceinline__ void warp_sort(uint32_t (&key)[K], int lane) {
+  constexpr int n = 32 * K;
+#pragma unroll
+  for (int k = 2; k <= n; k <<= 1) {
+#pragma unroll
+    for (int s = k >> 1; s > 0; s >>= 1) {
+      if (s >= 32) {  // partner in another register of this lane
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int pj = j ^ (s / 32);
+          if (pj > j) {
+            const int i = j * 32 + lane;
+            const bool up = (i & k) == 0;
+            const uint32_t a = key[j], b = key[pj];
+            const bool swap = up ? (a > b) : (a < b);
+            key[j] = swap ? b : a;
+            key[pj] = swap ? a : b;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int i = j * 32 + lane;
+          const uint32_t o = __shfl_xor_sync(kFull, key[j], s);
+          const bool up = (i & k) == 0;
+          const bool lower = (lane & s) == 0;
+          key[j] = (lower == up) ? (key[j] < o ? key[j] : o) : (key[j] > o ? key[j] : o);
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T lane_sentinel(int lane) {
+  return static_cast<T>(-1 - lane);
+}
+
+// Exact clipped counts of the S listed elements (one warp; etok / eps hold the
+// list, 1 <= S <= kSparseMax).  Returns order n's clipped count in lane n-1.
+template <typename T>
+__device__ __noinline__ unsigned int exact_counts(T* etok, uint32_t* eps, uint32_t* ekey, uint8_t* eid1,
+                                                  uint8_t* epid, uint8_t* eval, uint16_t* town, uint32_t* tcnt,
+                                                  int S, int R, int N, int lane) {
+  unsigned int hits = 0;
+  if (S > 0 && S <= 32) {
+    uint32_t key[1] = {lane < S ? elem_key(eps[lane] >> 16, eps[lane] & 0xffffu, lane) : 0xffffffffu};
+    warp_sort<1>(key, lane);
+    const bool v = lane < S;
+    const int e = static_cast<int>(key[0] & 127u);
+    const int side = v ? static_cast<int>(key[0] >> 23) : 15;
+    const int pos = static_cast<int>((key[0] >> 7) & 0xffffu);
+    const T tk = v ? etok[e] : lane_sentinel<T>(lane);
+    using MT = typename std::conditional<sizeof(T) == 4, unsigned int, unsigned long long>::type;
+    unsigned peers = __match_any_sync(kFull, static_cast<MT>(tk));
+    auto clip = [&](unsigned pr, bool valid, unsigned& c, unsigned& x) {
+      const unsigned vb = __ballot_sync(kFull, valid);
+      c = __popc(pr & vb & __ballot_sync(kFull, side == 0));
+      x = 0;
+      for (int r = 1; r <= R; ++r) {
+        const unsigned xr = __popc(pr & vb & __ballot_sync(kFull, side == r));
+        x = xr > x ? xr : x;
+      }
+    };
+    unsigned c, x;
+    clip(peers, v, c, x);
+    int leader = __ffs(peers) - 1;
+    unsigned h = (v && lane == leader) ? (c < x ? c : x) : 0u;
+    h = __reduce_add_sync(kFull, h);
+    if (lane == 0) hits = h;
+    bool valid = v && (side == 0 ? x > 0 : c > 0);  // its token matched: live at order 1
+    const int id1 = leader;
+    // the next element is the next position of the same row
+    const int pos_nx = __shfl_down_sync(kFull, pos, 1);
+    const int side_nx = __shfl_down_sync(kFull, side, 1);
+    const bool consec = lane + 1 < S && side_nx == side && pos_nx == pos + 1;
+    int pid = leader;
+    for (int n = 2; n <= N; ++n) {
+      if (!__any_sync(kFull, valid && side == 0)) break;  // no candidate (n-1)-gram matched
+      const bool up = __shfl_down_sync(kFull, valid, 1);
+      const int last = __shfl_sync(kFull, id1, (lane + n - 1) & 31);
+      valid = valid && consec && up;
+      const unsigned nkey = valid ? static_cast<unsigned>(pid * 32 + last) : 1024u + lane;
+      peers = __match_any_sync(kFull, nkey);
+      clip(peers, valid, c, x);
+      leader = __ffs(peers) - 1;
+      h = (valid && lane == leader) ? (c < x ? c : x) : 0u;
+      h = __reduce_add_sync(kFull, h);
+      if (lane == n - 1) hits = h;
+      valid = valid && (side == 0 ? x > 0 : c > 0);
+      pid = leader;
+    }
+  } else if (S > 32) {
+    // sort, rewrite the list in (row, position) order, then a tiny table per order
+    constexpr int kJ = kSparseMax / 32;
+    const int W = (R + 1 + 3) >> 2;  // count words per owner: 8-bit count per row
+    uint32_t key[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int e = j * 32 + lane;
+      key[j] = e < S ? elem_key(eps[e] >> 16, eps[e] & 0xffffu, e) : 0xffffffffu;
+    }
+    warp_sort<kJ>(key, lane);
+    T tj[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) tj[j] = j * 32 + lane < S ? etok[key[j] & 127u] : T(0);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int e = j * 32 + lane;
+      if (e < S) {
+        etok[e] = tj[j];
+        eps[e] = ((key[j] >> 23) << 16) | ((key[j] >> 7) & 0xffffu);
+      }
+    }
+    uint32_t own_e[kJ];
+    for (int i = lane; i < kTinySlots / 2; i += 32) reinterpret_cast<uint32_t*>(town)[i] = 0xffffffffu;
+    for (int i = lane; i < S * W; i += 32) tcnt[i] = 0;
+    __syncwarp();
+    // order 1: keys are the tokens
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int e = lane + 32 * j;
+      own_e[j] = 0xffffu;
+      if (e < S) {
+        const T tk = etok[e];
+        uint32_t s = tok_hash32(tk) >> 24;
+        uint16_t o;
+        while (true) {
+          uint16_t seen;
+          if (cas16(town, s, static_cast<uint16_t>(e), &seen)) {
+            o = static_cast<uint16_t>(e);
+            break;
+          }
+          if (etok[seen] == tk) {
+            o = seen;
+            break;
+          }
+          s = (s + 1) & (kTinySlots - 1);
+        }
+        own_e[j] = o;
+        const int side = static_cast<int>(eps[e] >> 16);
+        atomicAdd(&tcnt[o * W + (side >> 2)], 1u << (8 * (side & 3)));
+      }
+    }
+    __syncwarp();
+    auto counts = [&](uint32_t o, unsigned& c, unsigned& x) {
+      c = tcnt[o * W] & 0xffu;
+      x = 0;
+      for (int s = 1; s <= R; ++s) {
+        const unsigned xs = (tcnt[o * W + (s >> 2)] >> (8 * (s & 3))) & 0xffu;
+        x = xs > x ? xs : x;
+      }
+    };
+    unsigned acc = 0;
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int e = lane + 32 * j;
+      if (e < S) {
+        unsigned c, x;
+        counts(own_e[j], c, x);
+        if (own_e[j] == static_cast<uint32_t>(e)) acc += c < x ? c : x;
+        const int side = static_cast<int>(eps[e] >> 16);
+        eval[e] = (side == 0 ? x > 0 : c > 0) ? 1 : 0;
+        eid1[e] = static_cast<uint8_t>(own_e[j]);
+        epid[e] = static_cast<uint8_t>(own_e[j]);
+      }
+    }
+    acc = __reduce_add_sync(kFull, acc);
+    if (lane == 0) hits = acc;
+    __syncwarp();
+    for (int n = 2; n <= N; ++n) {
+      // (a) keys of the valid order-n elements
+      bool any_c = false;
+      bool vj[kJ];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int e = lane + 32 * j;
+        vj[j] = false;
+        if (e + 1 < S && eval[e] && eval[e + 1]) {
+          const uint32_t a = eps[e], nx = eps[e + 1];
+          // the next element is the next position of the same row and its
+          // (n-1)-gram matched too
+          vj[j] = (nx >> 16) == (a >> 16) && (nx & 0xffffu) == (a & 0xffffu) + 1;
+        }
+        if (vj[j]) any_c |= (eps[e] >> 16) == 0;
+        ekey[e] = vj[j] ? (static_cast<uint32_t>(epid[e]) << 8) | eid1[e + n - 1] : 0xffffffffu;
+      }
+      if (!__any_sync(kFull, any_c)) break;
+      for (int i = lane; i < kTinySlots / 2; i += 32) reinterpret_cast<uint32_t*>(town)[i] = 0xffffffffu;
+      for (int i = lane; i < S * W; i += 32) tcnt[i] = 0;
+      __syncwarp();
+      // (b) insert / count
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int e = lane + 32 * j;
+        own_e[j] = 0xffffu;
+        if (vj[j]) {
+          const uint32_t k2 = ekey[e];
+          uint32_t s = (k2 * 0x9E3779B1u) >> 24;
+          uint16_t o;
+          while (true) {
+            uint16_t seen;
+            if (cas16(town, s, static_cast<uint16_t>(e), &seen)) {
+              o = static_cast<uint16_t>(e);
+              break;
+            }
+            if (ekey[seen] == k2) {
+              o = seen;
+              break;
+            }
+            s = (s + 1) & (kTinySlots - 1);
+          }
+          own_e[j] = o;
+          const int side = static_cast<int>(eps[e] >> 16);
+          atomicAdd(&tcnt[o * W + (side >> 2)], 1u << (8 * (side & 3)));
+        }
+      }
+      __syncwarp();
+      // (c) clipped counts; the matched stay valid; ids for the next order
+      acc = 0;
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int e = lane + 32 * j;
+        if (e < S) {
+          bool nv = false;
+          if (vj[j]) {
+            unsigned c, x;
+            counts(own_e[j], c, x);
+            if (own_e[j] == static_cast<uint32_t>(e)) acc += c < x ? c : x;
+            nv = (eps[e] >> 16) == 0 ? x > 0 : c > 0;
+            epid[e] = static_cast<uint8_t>(own_e[j]);
+          }
+          eval[e] = nv ? 1 : 0;
+        }
+      }
+      acc = __reduce_add_sync(kFull, acc);
+      if (lane == n - 1) hits = acc;
+      __syncwarp();
+    }
+  }
+
+  return hits;
+}
 
 }  // namespace

@@ -41,9 +41,10 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
   int dev = 0;
   TB_CUDA(cudaGetDevice(&dev));
   if (attr_set[dev & 63] < pl.smem_bytes + 1) {
-    if (pl.smem_bytes > 48 * 1024)
-      TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(pl.smem_bytes)));
+    // (always: static + dynamic shared memory above 48 KiB needs the opt-in even
+    // when the dynamic part alone is below it)
+    TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(pl.smem_bytes)));
     // one shared-memory carveout for every stats kernel (no reconfiguration
     // between back-to-back launches of different kernels)
     if (!getenv("TB_DEBUG_NO_CARVEOUT"))
