@@ -439,8 +439,15 @@ int launch_sparse(const StatsParams& prm_in, int sms, cudaStream_t stream, int t
   int occ = 0;
   for (auto& e : cache)
     if (e.occ > 0 && e.k == reinterpret_cast<const void*>(kern) && e.dev == dev && e.smem == smem) occ = e.occ;
-  if (occ == 0) {
+  // the dynamic shared-memory opt-in of each kernel only ever grows (a smaller
+  // value set for one shape would refuse a larger cached shape later)
+  static size_t attr_max[4][64] = {};
+  size_t& amax = attr_max[(token_bytes == 4 ? 0 : 2) + (threads == 256 ? 0 : 1)][dev & 63];
+  if (smem > amax) {
     TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    amax = smem;
+  }
+  if (occ == 0) {
     // one shared-memory carveout for every stats kernel: back-to-back launches
     // of different kernels then need no L1/shared reconfiguration
     TB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
