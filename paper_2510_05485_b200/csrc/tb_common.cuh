@@ -114,6 +114,7 @@ struct StatsParams {
   // PCIe); report flags through the completion protocol with a plain store
   int prefix_only;
   int err_store;
+  int no_tails;  // every row is taken whole by the bulk copies: copy_row_tails has nothing to do
   // warp-group kernel: per-group shared-memory bytes, byte offsets, and the
   // element offsets of the staged rows (candidate, then reference r)
   int sp_off_fc, sp_off_fs, sp_off_tok, sp_off_ps, sp_off_aux, sp_off_rows;
@@ -608,6 +609,9 @@ inline int set_phase_buffer_here(void* buf) {
   return TB_OK;
 }
 #endif
+
+// 1 << (s & 31) in one funnel shift
+__device__ __forceinline__ uint32_t bit_of(uint32_t s) { return __funnelshift_l(1u, 1u, s); }
 
 template <typename T>
 __device__ __forceinline__ uint32_t tok_hash32(T t) {

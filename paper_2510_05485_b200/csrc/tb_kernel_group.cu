@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       s_nins[tid] = 0;
     }
     if (tid < 2 * R) s_nlr[tid / R][tid % R] = 0;
-    copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
+    if (!p.no_tails) copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
     // clear the table (entries EMPTY, reference counts 0); later orders clear only used slots
     for (uint32_t s = tid; s < cap / 4; s += kThreads) reinterpret_cast<uint4*>(ent)[s] = make_uint4(~0u, ~0u, ~0u, ~0u);
     for (uint32_t s = tid; s < cap / 8; s += kThreads) {

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
       s_len[tid] = l;
     }
     if (tid < N) s_hits[tid] = 0;
-    copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, NT);  // tails / unaligned rows
+    if (!p.no_tails) copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, NT);  // tails / unaligned rows
     mbar_wait(mbar, phase);
     phase ^= 1;
     __syncthreads();

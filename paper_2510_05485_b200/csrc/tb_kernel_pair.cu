@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
       s_ndef = 0;
       s_nf = 0;
     }
-    copy_row_tails<T>(p, b, 2, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
+    if (!p.no_tails) copy_row_tails<T>(p, b, 2, tok, s_stage_len, tid, kThreads);  // tails / unaligned rows
     // the table region starts as the two filter bitmaps (zero; they extend over
     // the count array) or as the empty table
     if (try_filter) {
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
       const uint32_t wshift = 32 - p.filter_log2;
       auto fmask = [](uint32_t h) {
         const uint32_t g = h * 0x85EBCA6Bu;
-        return (1u << (g >> 27)) | (1u << ((g >> 22) & 31u));
+        return bit_of(g >> 27) | bit_of(g >> 22);
       };
       for (int qi = tid; qi < nq; qi += kThreads) {
         int p0;

@@ -39,7 +39,6 @@ constexpr int kFsWords = 512;    // Fs: 16384 bits
 
 // Filters: word from the top bits of h = tok_hash32(t), bit from its low five
 // bits; bit_of(s) = 1 << (s & 31) in one funnel shift.
-__device__ __forceinline__ uint32_t bit_of(uint32_t s) { return __funnelshift_l(1u, 1u, s); }
 
 // Four tokens of a row at positions q..q+3 (q multiple of 4, q < len).  Vector
 // loads when the row is 16-byte aligned and q+4 <= width (the row's padding is

@@ -564,6 +564,15 @@ static int stats_impl(int32_t token_bytes, const void* cand_ids, int64_t cand_ld
   prm.gtab_stride = pl.gtab_stride;
   prm.prefix_only = prefix_only && pl.smem_mode;
   prm.err_store = err_store;
+  {  // full-width bulk copies take every row whole when bases, pitches and widths are 16-byte multiples
+    auto whole = [&](const void* base, int64_t ld, int64_t width) {
+      return (reinterpret_cast<uintptr_t>(base) & 15) == 0 && ((ld * token_bytes) & 15) == 0 &&
+             ((width * token_bytes) & 15) == 0;
+    };
+    bool nt = !prm.prefix_only && whole(cand_ids, cand_ld, cand_width);
+    for (int r = 0; r < num_refs && nt; ++r) nt = whole(ref_ids[r], ref_ld[r], ref_width[r]);
+    prm.no_tails = nt ? 1 : 0;
+  }
   if (pl.sparse) {
     prm.gcount = reinterpret_cast<unsigned int*>(ws + pl.list_off);
     prm.glist = reinterpret_cast<int*>(ws + pl.list_off + 16);
