@@ -45,10 +45,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   const int roff = cpad;  // first reference position (multiple of 4)
 
   uint64_t* mbars = reinterpret_cast<uint64_t*>(smem);  // one mbarrier per token buffer
-  T* const tokb[2] = {reinterpret_cast<T*>(smem + 16), reinterpret_cast<T*>(smem + p.off_tok2)};
+  // token buffer `buf` (computed from smem, not read from an array of pointers:
+  // a pointer array lives in local memory and every token access through it
+  // compiles to a generic LD/ST instead of LDS/STS)
+  auto tok_buf = [&](int buf) { return reinterpret_cast<T*>(smem + (buf ? p.off_tok2 : 16)); };
   const bool dbuf = p.off_tok2 != 0;  // prefetch the next group into the other buffer
   int cur = 0;
-  T* tok = tokb[0];
+  T* tok = tok_buf(0);
   uint32_t* kc = reinterpret_cast<uint32_t*>(tok);                 // aliases tok (orders >= 2)
   uint16_t* id1 = reinterpret_cast<uint16_t*>(smem + p.off_id1);   // order-1 slot; 0xffff: token unmatched
   uint16_t* idn = reinterpret_cast<uint16_t*>(smem + p.off_idn);   // order-n slot; 0xffff: n-gram unmatched
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   const uint32_t mask = cap - 1;
 
   auto issue_stage = [&](int64_t b, int buf) {
-    if (tid == 0) issue_rows<T>(p, b, 2, tokb[buf], mbars + buf, s_stage_len, &s_flags);
+    if (tid == 0) issue_rows<T>(p, b, 2, tok_buf(buf), mbars + buf, s_stage_len, &s_flags);
   };
 
   if (tid < 2 * N + 2) s_tot[tid] = 0;
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
 
   for (int64_t gi = blockIdx.x; gi < nb; gi += gridDim.x) {
     const int64_t b = group_at(gi);
-    tok = tokb[cur];
+    tok = tok_buf(cur);
     kc = reinterpret_cast<uint32_t*>(tok);
     if (p.prefix_only) {
       __syncthreads();  // s_stage_len of this group, written by thread 0 in issue_rows
@@ -189,12 +192,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
         T t[4];
         load4(p0, t);
         uint32_t* bm = p0 < roff ? bmc : bmr;
+        // branch-free: a position past the row's length ORs nothing
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (vm >> k & 1u) {
-            const uint32_t h = tok_hash32(t[k]);
-            atomicOr(&bm[h >> wshift], fmask(h));
-          }
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t h = tok_hash32(t[k]);
+          atomicOr(&bm[h >> wshift], (vm >> k & 1u) ? fmask(h) : 0u);
+        }
       }
       __syncthreads();
       TB_MARK(20);
@@ -206,12 +209,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
         const uint32_t* bm = p0 < roff ? bmr : bmc;  // the other side's
         uint32_t pm = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (vm >> k & 1u) {
-            const uint32_t h = tok_hash32(t[k]);
-            const uint32_t m = fmask(h);
-            if ((bm[h >> wshift] & m) == m) pm |= 1u << k;
-          }
+        for (int k = 0; k < 4; ++k) {  // branch-free; positions past the length masked below
+          const uint32_t h = tok_hash32(t[k]);
+          const uint32_t m = fmask(h);
+          pm |= ((bm[h >> wshift] & m) == m ? 1u : 0u) << k;
+        }
+        pm &= vm;
         // every valid position starts "unmatched" at order 1 (the exact match below
         // marks the matched ones)
         *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
