@@ -661,10 +661,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
             if (i0 >= roff || x != 0) lm |= 1u << k;
           }
         }
-        // the quads of a warp can straddle the two parts: one append per part
+        // the quads of (at most) one warp straddle the two parts: one append per part there
         const bool cside = qi < mcq;
-        warp_append_quad(lout, &s_nc, cside ? lm : 0u, [&](int k) { return pos[k]; }, lane);
-        warp_append_quad(lout + roff, &s_nr, cside ? 0u : lm, [&](int k) { return pos[k]; }, lane);
+        const unsigned cs = __ballot_sync(kFull, cside);
+        if (cs != 0u) warp_append_quad(lout, &s_nc, cside ? lm : 0u, [&](int k) { return pos[k]; }, lane);
+        if (cs != kFull) warp_append_quad(lout + roff, &s_nr, cside ? 0u : lm, [&](int k) { return pos[k]; }, lane);
       }
       hits = __reduce_add_sync(kFull, hits);
       if (lane == 0 && hits) atomicAdd(&s_hits[n - 1], hits);
