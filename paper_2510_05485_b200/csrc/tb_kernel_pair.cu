@@ -182,10 +182,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
       uint32_t* bmc = reinterpret_cast<uint32_t*>(own);  // candidate tokens
       uint32_t* bmr = bmc + (1u << p.filter_log2);        // reference tokens
       const uint32_t wshift = 32 - p.filter_log2;
-      auto fmask = [](uint32_t h) {
-        const uint32_t g = h * 0x85EBCA6Bu;
-        return bit_of(g >> 27) | bit_of(g >> 22);
-      };
+// the two bits from the ten hash bits just below the word index (one
+      // product per token: h's top bits pick the word)
+      const uint32_t bs1 = wshift - 5, bs2 = wshift - 10;
+      auto fmask = [bs1, bs2](uint32_t h) { return bit_of(h >> bs1) | bit_of(h >> bs2); };
       for (int qi = tid; qi < nq; qi += kThreads) {
         int p0;
         const uint32_t vm = quad(qi, p0);
