@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
       uint32_t* bmc = reinterpret_cast<uint32_t*>(own);  // candidate tokens
       uint32_t* bmr = bmc + (1u << p.filter_log2);        // reference tokens
       const uint32_t wshift = 32 - p.filter_log2;
-// the two bits from the ten hash bits just below the word index (one
+      // the two bits from the ten hash bits just below the word index (one
       // product per token: h's top bits pick the word)
       const uint32_t bs1 = wshift - 5, bs2 = wshift - 10;
       auto fmask = [bs1, bs2](uint32_t h) { return bit_of(h >> bs1) | bit_of(h >> bs2); };
