@@ -21,7 +21,7 @@ namespace {
 // NT threads per CTA: 256 (4 CTAs per SM) for batches of many groups, 512
 // (2 per SM) when the batch is one wave: every phase then has half the work per
 // thread, which is the per-group latency the step waits for.
-template <typename T, int NT, bool kList>
+template <typename T, int NT, bool kList, bool kThree>
 __global__ void __launch_bounds__(NT, 1024 / NT)
     bleu_pair_kernel(const __grid_constant__ StatsParams p) {
   constexpr int kThreads = NT;
@@ -89,6 +89,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   // off after a group of this CTA needed the hash passes (related text); listed
   // groups are known to need them
   bool try_filter = !kList;
+  // Rows of more quads than threads filter in three passes (candidate tokens
+  // into Fc, reference tokens against it, candidate tokens against the small
+  // filter of the reference survivors): one loop iteration per thread and
+  // pass instead of two over both rows.  Short rows keep the two passes.  A
+  // template parameter: both paths in one kernel cost c2 0.1 us and c4 0.5 us.
+  constexpr bool three_pass = kThree;
 
   for (int64_t gi = blockIdx.x; gi < nb; gi += gridDim.x) {
     const int64_t b = group_at(gi);
@@ -119,7 +125,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     // the table region starts as the two filter bitmaps (zero; they extend over
     // the count array) or as the empty table
     if (try_filter) {
-      for (uint32_t s = tid; s < (1u << p.filter_log2) / 2; s += kThreads)
+      // two-pass: both sides' bitmaps; three-pass: Fc and the small filter after it
+      const uint32_t fwords = three_pass ? (1u << p.filter_log2) + (1u << min(p.filter_log2, 8))
+                                         : 2u << p.filter_log2;
+      for (uint32_t s = tid; s < fwords / 4; s += kThreads)
         reinterpret_cast<uint4*>(own)[s] = make_uint4(0, 0, 0, 0);
     } else {
       for (uint32_t s = tid; s < cap / 8; s += kThreads)
@@ -186,47 +195,117 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
       // product per token: h's top bits pick the word)
       const uint32_t bs1 = wshift - 5, bs2 = wshift - 10;
       auto fmask = [bs1, bs2](uint32_t h) { return bit_of(h >> bs1) | bit_of(h >> bs2); };
-      for (int qi = tid; qi < nq; qi += kThreads) {
-        int p0;
-        const uint32_t vm = quad(qi, p0);
-        T t[4];
-        load4(p0, t);
-        uint32_t* bm = p0 < roff ? bmc : bmr;
-        // branch-free: a position past the row's length ORs nothing
+      if (three_pass) {
+        // Three passes: candidate tokens into Fc; reference tokens tested
+        // against Fc — the survivors are listed and marked in a small filter Fs
+        // (<= 256 words) — and candidate tokens tested against Fs only
+        // while the list still fits (related text stops after the second).
+        uint32_t* const fsm = bmr;  // Fs, in the (otherwise unused) reference half
+        const uint32_t tl = p.filter_log2 < 8 ? p.filter_log2 : 8;  // Fs: 2^tl words
+        auto smask = [tl](uint32_t h) { return bit_of(h >> (27 - tl)) | bit_of(h >> (22 - tl)); };
+        for (int qi = tid; qi < ncq; qi += kThreads) {
+          const int p0 = 4 * qi;
+          const uint32_t vm = clen - p0 >= 4 ? 0xfu : ((1u << (clen - p0)) - 1u);
+          T t[4];
+          load4(p0, t);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t h = tok_hash32(t[k]);
-          atomicOr(&bm[h >> wshift], (vm >> k & 1u) ? fmask(h) : 0u);
+          for (int k = 0; k < 4; ++k) {  // branch-free: a position past the length ORs nothing
+            const uint32_t h = tok_hash32(t[k]);
+            atomicOr(&bmc[h >> wshift], (vm >> k & 1u) ? fmask(h) : 0u);
+          }
         }
-      }
-      __syncthreads();
-      TB_MARK(20);
-      for (int qi = tid; qi < nq; qi += kThreads) {
-        int p0;
-        const uint32_t vm = quad(qi, p0);
-        T t[4];
-        load4(p0, t);
-        const uint32_t* bm = p0 < roff ? bmr : bmc;  // the other side's
-        uint32_t pm = 0;
+        __syncthreads();
+        TB_MARK(20);
+        const int nrq = nq - ncq;
+        for (int qi = tid; qi < nrq; qi += kThreads) {
+          const int p0 = roff + 4 * qi;
+          const uint32_t vm = roff + rlen - p0 >= 4 ? 0xfu : ((1u << (roff + rlen - p0)) - 1u);
+          T t[4];
+          load4(p0, t);
+          uint32_t pm = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // branch-free; positions past the length masked below
-          const uint32_t h = tok_hash32(t[k]);
-          const uint32_t m = fmask(h);
-          pm |= ((bm[h >> wshift] & m) == m ? 1u : 0u) << k;
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t h = tok_hash32(t[k]);
+            const uint32_t m = fmask(h);
+            pm |= ((bmc[h >> wshift] & m) == m ? 1u : 0u) << k;
+          }
+          pm &= vm;
+          *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
+          *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
+          for (; pm; pm &= pm - 1) {
+            const int k = __ffs(pm) - 1;
+            const int j = atomicAdd(&s_nf, 1);
+            if (j < kSmallSet) s_flist[j] = static_cast<uint16_t>(p0 + k);
+            const uint32_t h = tok_hash32(tok[p0 + k]);
+            atomicOr(&fsm[h >> (32 - tl)], smask(h));
+          }
         }
-        pm &= vm;
-        // every valid position starts "unmatched" at order 1 (the exact match below
-        // marks the matched ones)
-        *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
-        *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
-        // (an early exit once more survivors than the exact match takes were
-        // listed — related text — saved 1.8 us at c2 related but cost 0.5 us
-        // at c2 uniform: the loop stays branch-free)
-        for (; pm; pm &= pm - 1) {
-          const int j = atomicAdd(&s_nf, 1);
-          if (j < kSmallSet) s_flist[j] = static_cast<uint16_t>(p0 + __ffs(pm) - 1);
+        __syncthreads();
+        if (s_nf <= kSmallSet) {  // uniform across the CTA
+          for (int qi = tid; qi < ncq; qi += kThreads) {
+            const int p0 = 4 * qi;
+            const uint32_t vm = clen - p0 >= 4 ? 0xfu : ((1u << (clen - p0)) - 1u);
+            T t[4];
+            load4(p0, t);
+            uint32_t pm = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t h = tok_hash32(t[k]);
+              const uint32_t m = smask(h);
+              pm |= ((fsm[h >> (32 - tl)] & m) == m ? 1u : 0u) << k;
+            }
+            pm &= vm;
+            *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
+            *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
+            for (; pm; pm &= pm - 1) {
+              const int j = atomicAdd(&s_nf, 1);
+              if (j < kSmallSet) s_flist[j] = static_cast<uint16_t>(p0 + __ffs(pm) - 1);
+            }
+          }
         }
+      } else {
+        for (int qi = tid; qi < nq; qi += kThreads) {
+          int p0;
+          const uint32_t vm = quad(qi, p0);
+          T t[4];
+          load4(p0, t);
+          uint32_t* bm = p0 < roff ? bmc : bmr;
+          // branch-free: a position past the row's length ORs nothing
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t h = tok_hash32(t[k]);
+            atomicOr(&bm[h >> wshift], (vm >> k & 1u) ? fmask(h) : 0u);
+          }
+        }
+        __syncthreads();
+        TB_MARK(20);
+        for (int qi = tid; qi < nq; qi += kThreads) {
+          int p0;
+          const uint32_t vm = quad(qi, p0);
+          T t[4];
+          load4(p0, t);
+          const uint32_t* bm = p0 < roff ? bmr : bmc;  // the other side's
+          uint32_t pm = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // branch-free; positions past the length masked below
+            const uint32_t h = tok_hash32(t[k]);
+            const uint32_t m = fmask(h);
+            pm |= ((bm[h >> wshift] & m) == m ? 1u : 0u) << k;
+          }
+          pm &= vm;
+          // every valid position starts "unmatched" at order 1 (the exact match below
+          // marks the matched ones)
+          *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
+          *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
+          // (an early exit once more survivors than the exact match takes were
+          // listed — related text — saved 1.8 us at c2 related but cost 0.5 us
+          // at c2 uniform: the loop stays branch-free)
+          for (; pm; pm &= pm - 1) {
+            const int j = atomicAdd(&s_nf, 1);
+            if (j < kSmallSet) s_flist[j] = static_cast<uint16_t>(p0 + __ffs(pm) - 1);
+          }
 
+        }
       }
       __syncthreads();
       TB_MARK(21);
@@ -760,15 +839,21 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
 namespace tbk {
 
 int launch_pair(const StatsParams& prm, const Plan& pl, int sms, cudaStream_t stream, int token_bytes) {
-  static size_t attr_set[4][64] = {};
+  static size_t attr_set[6][64] = {};
   // (512-thread CTAs, bleu_pair_kernel<T, 512, .>, measured no faster on single
   // waves of few groups: c1 5.48 vs 5.60 us; 256 everywhere)
-  const bool list = prm.glist != nullptr;  // the groups listed by the filter kernel
-  if (token_bytes == 4)
-    return list ? launch_kernel(bleu_pair_kernel<int32_t, 256, true>, prm, pl, sms, true, attr_set[2], stream)
-                : launch_kernel(bleu_pair_kernel<int32_t, 256, false>, prm, pl, sms, true, attr_set[0], stream);
-  return list ? launch_kernel(bleu_pair_kernel<int64_t, 256, true>, prm, pl, sms, true, attr_set[3], stream)
-              : launch_kernel(bleu_pair_kernel<int64_t, 256, false>, prm, pl, sms, true, attr_set[1], stream);
+  const bool list = prm.glist != nullptr;  // the groups listed by the filter kernel (no filter passes)
+  // three-pass filter when the two rows hold more quads than a CTA has threads
+  // (c2 7.06 -> 6.85 us, c4 33.8 -> 33.0; c1's 256-token rows 5.09 vs 5.45 two-pass)
+  const bool three = (static_cast<int64_t>(prm.cand_pad) + prm.ref_off[1]) / 4 > 256;
+  if (token_bytes == 4) {
+    if (list) return launch_kernel(bleu_pair_kernel<int32_t, 256, true, false>, prm, pl, sms, true, attr_set[2], stream);
+    return three ? launch_kernel(bleu_pair_kernel<int32_t, 256, false, true>, prm, pl, sms, true, attr_set[4], stream)
+                 : launch_kernel(bleu_pair_kernel<int32_t, 256, false, false>, prm, pl, sms, true, attr_set[0], stream);
+  }
+  if (list) return launch_kernel(bleu_pair_kernel<int64_t, 256, true, false>, prm, pl, sms, true, attr_set[3], stream);
+  return three ? launch_kernel(bleu_pair_kernel<int64_t, 256, false, true>, prm, pl, sms, true, attr_set[5], stream)
+               : launch_kernel(bleu_pair_kernel<int64_t, 256, false, false>, prm, pl, sms, true, attr_set[1], stream);
 }
 
 #ifdef TB_PHASES
