@@ -37,6 +37,9 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
   __shared__ uint8_t s_sside[kSmallSet];   // small-set path: 0 = candidate, 1 + r = reference r
   __shared__ int64_t s_effref;             // effective reference length of the current group
   __shared__ double s_bp;                  // and its brevity penalty
+  __shared__ uint16_t s_flist[kSmallSet];  // order-1 filter survivors (positions)
+  __shared__ T s_ftok[kSmallSet];          // and their tokens
+  __shared__ int s_nf;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -83,6 +86,17 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
   __syncthreads();
   TB_MARK(0);
   uint32_t phase = 0;
+  // The order-1 filter (below) is tried until a group of this CTA needs the
+  // hash passes (related text; listed groups are known to), and only when
+  // every CTA has two or more groups: with one group per CTA a group of
+  // related text pays the whole failed filter (c3 related 43.9 -> 47.6 us,
+  // against c3 uniform 15.1 -> 12.3 us); with more, one failure per CTA.
+  bool try_filter = !kList && nb >= 2 * static_cast<int64_t>(gridDim.x);
+  // Fc: a blocked two-bit Bloom filter of the candidate tokens in the first
+  // half of the table region (2^fl words), Fs: the reference survivors' filter
+  // after it (2^tl <= 256 words)
+  const int fl = cap_log2 - 2;
+  const uint32_t tl = fl < 8 ? fl : 8;
 
   for (int64_t gi = blockIdx.x; gi < nb; gi += gridDim.x) {
     const int64_t b = group_at(gi);
@@ -100,7 +114,15 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
       s_len[tid] = l;
     }
     if (tid < N) s_hits[tid] = 0;
+    if (tid == 0) {
+      s_nf = 0;
+      s_nc = 0;
+      s_nr = 0;
+    }
     if (!p.no_tails) copy_row_tails<T>(p, b, R + 1, tok, s_stage_len, tid, NT);  // tails / unaligned rows
+    if (try_filter)
+      for (uint32_t s = tid; s < ((1u << fl) + (1u << tl)) / 4; s += NT)
+        reinterpret_cast<uint4*>(own)[s] = make_uint4(0, 0, 0, 0);
     mbar_wait(mbar, phase);
     phase ^= 1;
     __syncthreads();
@@ -351,8 +373,162 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
       __syncthreads();
     };
 
+    // ================= order 1: filter =================
+    // Unrelated text: three Bloom passes — candidate tokens into Fc, every
+    // reference's tokens tested against Fc (survivors listed and marked in
+    // Fs), candidate tokens tested against Fs — leave the few positions whose
+    // token may occur on the other side.  When at most kSmallSet do, the block
+    // matches them exactly (per-reference counts, clip min(c, max_r x_r)),
+    // gives each live position its order-1 id (the lowest list index holding
+    // its token) and the small-set path below finishes orders >= 2: no table.
+    bool filtered = false;
+    if (try_filter) {
+      uint32_t* const fc = reinterpret_cast<uint32_t*>(own);
+      uint32_t* const fsm = fc + (1u << fl);
+      const uint32_t wshift = 32 - fl, bs1 = wshift - 5, bs2 = wshift - 10;
+      auto fmask = [bs1, bs2](uint32_t h) { return bit_of(h >> bs1) | bit_of(h >> bs2); };
+      auto smask = [tl](uint32_t h) { return bit_of(h >> (27 - tl)) | bit_of(h >> (22 - tl)); };
+      auto load4 = [&](int p0, T (&t)[4]) {
+        if constexpr (sizeof(T) == 4) {
+          const int4 v = *reinterpret_cast<const int4*>(tok + p0);
+          t[0] = v.x;
+          t[1] = v.y;
+          t[2] = v.z;
+          t[3] = v.w;
+        } else {
+          const longlong2 u = *reinterpret_cast<const longlong2*>(tok + p0);
+          const longlong2 v = *reinterpret_cast<const longlong2*>(tok + p0 + 2);
+          t[0] = u.x;
+          t[1] = u.y;
+          t[2] = v.x;
+          t[3] = v.y;
+        }
+      };
+      auto list_survivors = [&](uint32_t pm, int p0, int side, bool mark) {
+        // once the list has overflowed (related text) the filter has failed:
+        // nothing more to list or mark (s_nf only grows)
+        if (pm == 0 || *reinterpret_cast<volatile int*>(&s_nf) > kSmallSet) return;
+        for (; pm; pm &= pm - 1) {
+          const int pos = p0 + __ffs(pm) - 1;
+          const int j = atomicAdd(&s_nf, 1);
+          const T tk = tok[pos];
+          if (j < kSmallSet) {
+            s_flist[j] = static_cast<uint16_t>(pos);
+            s_ftok[j] = tk;
+            s_sside[j] = static_cast<uint8_t>(side);  // 0 = candidate, 1 + r = reference r
+          }
+          if (mark) {
+            const uint32_t h = tok_hash32(tk);
+            atomicOr(&fsm[h >> (32 - tl)], smask(h));
+          }
+        }
+      };
+      for (int qi = tid; qi < ncq; qi += NT) {  // candidate tokens into Fc (branch-free)
+        const int p0 = 4 * qi;
+        const uint32_t vm = cand_mask(p0);
+        T t[4];
+        load4(p0, t);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t h = tok_hash32(t[k]);
+          atomicOr(&fc[h >> wshift], (vm >> k & 1u) ? fmask(h) : 0u);
+        }
+      }
+      if (tid == NT - 32) {  // lengths only: the last warp
+        const int64_t r = closest_ref_len(s_len[0], &s_len[1], R);
+        s_effref = r;
+        s_bp = brevity_penalty_fp64(s_len[0], r);
+      }
+      __syncthreads();
+      TB_MARK(20);
+      for (int qi = tid; qi < nrq; qi += NT) {  // reference tokens against Fc
+        int r, p0;
+        const uint32_t vm = ref_quad(qi, r, p0);
+        T t[4];
+        load4(p0, t);
+        uint32_t pm = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t h = tok_hash32(t[k]);
+          const uint32_t m = fmask(h);
+          pm |= ((fc[h >> wshift] & m) == m ? 1u : 0u) << k;
+        }
+        *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);  // unmatched unless listed live
+        *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
+        list_survivors(pm & vm, p0, 1 + r, true);
+      }
+      __syncthreads();
+      TB_MARK(21);
+      TB_NOTE(25, s_nf);
+      if (s_nf <= kSmallSet) {  // uniform
+        for (int qi = tid; qi < ncq; qi += NT) {  // candidate tokens against Fs
+          const int p0 = 4 * qi;
+          const uint32_t vm = cand_mask(p0);
+          T t[4];
+          load4(p0, t);
+          uint32_t pm = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t h = tok_hash32(t[k]);
+            const uint32_t m = smask(h);
+            pm |= ((fsm[h >> (32 - tl)] & m) == m ? 1u : 0u) << k;
+          }
+          *reinterpret_cast<uint2*>(id1 + p0) = make_uint2(~0u, ~0u);
+          *reinterpret_cast<uint2*>(idn + p0) = make_uint2(~0u, ~0u);
+          list_survivors(pm & vm, p0, 0, false);
+        }
+        __syncthreads();
+      }
+      TB_MARK(22);
+      const int S = s_nf;
+      TB_NOTE(27, S);
+      if (S <= kSmallSet) {
+        filtered = true;
+        if (tid < S) {  // exact order 1 among the listed positions
+          // branch-free scan of the list (every entry matches itself, so a
+          // branch per match would run on every iteration): the reference
+          // counts in eight 8-bit fields (<= kSmallSet = 128 each), the lowest
+          // index holding the token as its id
+          const int pos = s_flist[tid];
+          const T tk = s_ftok[tid];
+          const int side = s_sside[tid];
+          unsigned c = 0;
+          unsigned long long xr = 0;
+          int leader = tid;
+          for (int j = S - 1; j >= 0; --j) {
+            const bool eq = s_ftok[j] == tk;
+            const int sj = s_sside[j];
+            leader = eq ? j : leader;
+            c += (eq && sj == 0) ? 1u : 0u;
+            xr += (eq && sj != 0) ? (1ull << (8 * (sj - 1))) : 0ull;
+          }
+          unsigned x = 0;
+#pragma unroll
+          for (int r = 0; r < kMultiMaxRefs; ++r) {
+            const unsigned v = static_cast<unsigned>(xr >> (8 * r)) & 0xffu;
+            x = v > x ? v : x;
+          }
+          if (leader == tid) {
+            const unsigned h = c < x ? c : x;
+            if (h) atomicAdd(&s_hits[0], h);
+          }
+          if (side == 0 ? x > 0 : c > 0) {
+            id1[pos] = static_cast<uint16_t>(leader);
+            idn[pos] = static_cast<uint16_t>(leader);
+            if (side == 0) lx[atomicAdd(&s_nc, 1)] = static_cast<uint16_t>(pos);
+            else lx[cpad + atomicAdd(&s_nr, 1)] = static_cast<uint16_t>(pos);
+          }
+        }
+        TB_MARK(23);
+        __syncthreads();
+        TB_MARK(1);
+      } else {
+        try_filter = false;  // related text: the hash passes (uniform across the CTA)
+      }
+    }
+
     // ================= order 1: tokens =================
-    count_order1(static_cast<const T*>(tok), id1, idn);
+    if (!filtered) count_order1(static_cast<const T*>(tok), id1, idn);
     TB_MARK(4);
     int nc = s_nc, nr = s_nr;
 
@@ -572,22 +748,23 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
         bool ok = false;
         int leader = tid;
         if (valid) {
+          // branch-free (every entry matches itself): reference counts in
+          // eight 8-bit fields (<= kSmallSet each)
           unsigned c = 0;
-          unsigned xr[kMultiMaxRefs] = {0, 0, 0, 0, 0, 0, 0, 0};
-          for (int j = 0; j < S; ++j) {
-            if (s_skey[j] != key) continue;
-            leader = j < leader ? j : leader;
+          unsigned long long xr = 0;
+          for (int j = S - 1; j >= 0; --j) {
+            const bool eq = s_skey[j] == key;
             const int sj = s_sside[j];
-            if (sj == 0) {
-              ++c;
-            } else {
-#pragma unroll
-              for (int r = 0; r < kMultiMaxRefs; ++r) xr[r] += (sj == r + 1) ? 1u : 0u;
-            }
+            leader = eq ? j : leader;
+            c += (eq && sj == 0) ? 1u : 0u;
+            xr += (eq && sj != 0) ? (1ull << (8 * (sj - 1))) : 0ull;
           }
           unsigned x = 0;
 #pragma unroll
-          for (int r = 0; r < kMultiMaxRefs; ++r) x = xr[r] > x ? xr[r] : x;
+          for (int r = 0; r < kMultiMaxRefs; ++r) {
+            const unsigned v = static_cast<unsigned>(xr >> (8 * r)) & 0xffu;
+            x = v > x ? v : x;
+          }
           if (leader == tid) {
             const unsigned h = c < x ? c : x;
             if (h) atomicAdd(&s_hits[m - 1], h);

@@ -31,6 +31,7 @@ struct Plan {
 };
 
 constexpr size_t kStaticSmemReserve = 2048;  // static __shared__ of the stats kernels (upper bound)
+constexpr size_t kMultiStaticReserve = 3072;  // the multi-reference kernel's (its filter lists)
 constexpr int64_t kGlobalGridCap = 2 * 148;
 // fixed-size completion region at the start of the workspace, independent of N
 constexpr size_t kAccBytes = ((kAccCopies * (2 * TB_MAX_ORDER + 2) * 8 + 256) + 255) / 256 * 256;

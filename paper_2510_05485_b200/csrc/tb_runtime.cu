@@ -343,11 +343,11 @@ int make_plan(int64_t batch, int R, int64_t cand_width, const int64_t* ref_width
     int lg = cap_log2_for(8 * cpad4, 6);
     int64_t offs[6];
     int64_t total = multi_layout(lg, offs);
-    while (total + static_cast<int64_t>(kStaticSmemReserve) > smem_optin / 2 && (int64_t(1) << (lg - 1)) >= 2 * cpad4) {
+    while (total + static_cast<int64_t>(kMultiStaticReserve) > smem_optin / 2 && (int64_t(1) << (lg - 1)) >= 2 * cpad4) {
       --lg;
       total = multi_layout(lg, offs);
     }
-    if (lg <= 15 && ptot < 65535 && total + static_cast<int64_t>(kStaticSmemReserve) <= smem_optin) {
+    if (lg <= 15 && ptot < 65535 && total + static_cast<int64_t>(kMultiStaticReserve) <= smem_optin) {
       pl->smem_mode = true;
       pl->multi = true;
       pl->cand_pad = static_cast<int>(cpad4);
