@@ -33,7 +33,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--workload", default="c2")
     a = p.parse_args()
-    b, l, v, r, sm = bench.WORKLOADS[a.workload]
+    b, l, v, r, sm = bench.WORKLOADS[a.workload][:5]
     cand, refs = bench.generate_batch(b, l, v, r)
     cfg = tb.BleuConfig(smoothing=sm)
     hc = tb.TokenBatch(ids=torch.from_numpy(cand[0]).pin_memory(), lengths=torch.from_numpy(cand[1]))
@@ -66,7 +66,7 @@ def c2_native_vs_python():
     """tb_bleu_host at c2 through the native binding with prebuilt views vs
     the public sentence_bleu call (the difference is the Python layer)."""
     from paper_2510_05485_b200 import _native, bleu
-    b, l, v, r, sm = bench.WORKLOADS["c2"]
+    b, l, v, r, sm = bench.WORKLOADS["c2"][:5]
     cand, refs = bench.generate_batch(b, l, v, r)
     cfg = tb.BleuConfig(smoothing=sm)
     hc = tb.TokenBatch(ids=torch.from_numpy(cand[0].astype(np.int32)).pin_memory(), lengths=torch.from_numpy(cand[1]))
@@ -93,7 +93,7 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "native":
     c2_native_vs_python()
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ncu":
     from paper_2510_05485_b200 import _native, bleu
-    b, l, v, r, sm = bench.WORKLOADS["c2"]
+    b, l, v, r, sm = bench.WORKLOADS["c2"][:5]
     cand, refs = bench.generate_batch(b, l, v, r)
     cfg = tb.BleuConfig(smoothing=sm)
     hc = tb.TokenBatch(ids=torch.from_numpy(cand[0].astype(np.int32)).pin_memory(), lengths=torch.from_numpy(cand[1]))
