@@ -94,11 +94,6 @@ __device__ __forceinline__ void lds_quad(const T* src, T (&t)[4]) {
   }
 }
 
-// mask of the valid positions of quad q
-__device__ __forceinline__ uint32_t tail_mask(int q, int len) {
-  const int left = len - q;
-  return left >= 4 ? 0xfu : ((1u << left) - 1u);
-}
 
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT, (sizeof(T) == 4 ? 1024 : 768) / NT)
