@@ -663,34 +663,37 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
         uint32_t kw[4];
   #pragma unroll
         for (int k = 0; k < 4; ++k) kw[k] = w[k] != 0xffffu ? kc[w[k]] : ~0u;
-        if (i0 < roff) {
+        // predicated per entry (the branchy form spent a third of the related-text
+        // instructions on control flow): a candidate owning its slot or a key
+        // equal to its slot's records the slot id (+1 on the owner's count); a
+        // reference key with an EMPTY home is dead; the rest — candidates lost to
+        // a different key, references whose home holds another key — are rare
+        // and handled after the loop.  (A live candidate key's home is never
+        // empty: the claim pass stored into it.)
+        const bool rside = i0 >= roff;
+        uint32_t rare = 0;
   #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (key[k] == ~0u) continue;
-            const int i = i0 + k;
-            if (w[k] == i) {
-              idn[pos[k]] = static_cast<uint16_t>(i);
-            } else if (kw[k] == key[k]) {
-              atomicAdd(&cnt[w[k]], 1u);
-              idn[pos[k]] = w[k];
-            } else {
-              lout[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(i);
-              pair_retry_store(own, key[k] * 0x9E3779B1u, 1, hshift, static_cast<uint16_t>(i));
-            }
-          }
-        } else {
-  #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (key[k] == ~0u) continue;
-            const int i = i0 + k;
-            if (w[k] == 0xffffu) {  // empty home: no candidate n-gram has this key
-              kc[i] = ~0u;
-            } else if (kw[k] == key[k]) {
-              atomicAdd(&cnt[w[k]], 1u << 16);
-              idn[pos[k]] = w[k];
-            } else {
-              defl[atomicAdd(&s_ndef, 1)] = static_cast<uint16_t>(i);
-            }
+        for (int k = 0; k < 4; ++k) {
+          const int i = i0 + k;
+          const bool live = key[k] != ~0u;
+          const bool self = !rside && w[k] == i;
+          const bool hit = live && !self && kw[k] == key[k];
+          const bool empty = live && rside && w[k] == 0xffffu;
+          if (self || hit) idn[pos[k]] = static_cast<uint16_t>(w[k]);
+          // (constant increments: one atomic with a per-lane operand made
+          // vocab = 1 rows, every lane on one word, 12% slower)
+          if (hit && !rside) atomicAdd(&cnt[w[k]], 1u);
+          if (hit && rside) atomicAdd(&cnt[w[k]], 1u << 16);
+          if (empty) kc[i] = ~0u;
+          rare |= (live && !self && !hit && !empty ? 1u : 0u) << k;
+        }
+        for (; rare; rare &= rare - 1) {
+          const int i = i0 + __ffs(rare) - 1;
+          if (rside) {
+            defl[atomicAdd(&s_ndef, 1)] = static_cast<uint16_t>(i);
+          } else {
+            lout[atomicAdd(&s_nlost, 1)] = static_cast<uint16_t>(i);
+            pair_retry_store(own, kc[i] * 0x9E3779B1u, 1, hshift, static_cast<uint16_t>(i));
           }
         }
       }
@@ -732,12 +735,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
   #pragma unroll
           for (int k = 0; k < 4; ++k) cw[k] = key[k] != ~0u ? cnt[w[k]] : 0u;
   #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (key[k] == ~0u) continue;
+          for (int k = 0; k < 4; ++k) {  // (predicated)
+            const bool live = key[k] != ~0u;
             const uint32_t c = (cw[k] & 0xffffu) + 1u;  // owners are candidate entries
             const uint32_t x = cw[k] >> 16;
-            if (w[k] == static_cast<uint32_t>(i0 + k)) hits += c < x ? c : x;
-            if (i0 >= roff || x != 0) lm |= 1u << k;
+            hits += (live && w[k] == static_cast<uint32_t>(i0 + k)) ? (c < x ? c : x) : 0u;
+            lm |= (live && (i0 >= roff || x != 0) ? 1u : 0u) << k;
           }
         }
         // the quads of (at most) one warp straddle the two parts: one append per part there
