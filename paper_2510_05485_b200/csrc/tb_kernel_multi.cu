@@ -519,9 +519,7 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
             else lx[cpad + atomicAdd(&s_nr, 1)] = static_cast<uint16_t>(pos);
           }
         }
-        TB_MARK(23);
         __syncthreads();
-        TB_MARK(1);
       } else {
         try_filter = false;  // related text: the hash passes (uniform across the CTA)
       }
