@@ -794,20 +794,25 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     }
 
     TB_MARK(24);
-    // ---- epilogue (warp 0)
-    if (tid < 32) {
+    // ---- epilogue: warp 0 the fp64 scores, warp 1 (in parallel) the integer
+    // outputs; warp 1 waits on a named barrier for warp 0, the last writer of
+    // the counts (the orders >= 2 of few survivors)
+    if (tid < 64) {
+      asm volatile("bar.sync 1, 64;" ::: "memory");
       const int64_t c = s_len[0];
       const int64_t num = lane < N ? static_cast<int64_t>(s_hits[lane]) : 0;
       const int64_t den = (lane < N && c - lane > 0) ? c - lane : 0;
-      if (lane < N) {
-        if (p.num) p.num[b * N + lane] = num;
-        if (p.den) p.den[b * N + lane] = den;
-      }
       const int64_t r = s_len[1];
-      if (lane == 0) {
-        if (p.cand_len_out) p.cand_len_out[b] = c;
-        if (p.eff_ref) p.eff_ref[b] = r;
-      }
+      if (tid >= 32) {
+        if (lane < N) {
+          if (p.num) p.num[b * N + lane] = num;
+          if (p.den) p.den[b * N + lane] = den;
+        }
+        if (lane == 0) {
+          if (p.cand_len_out) p.cand_len_out[b] = c;
+          if (p.eff_ref) p.eff_ref[b] = r;
+        }
+      } else {
       if (p.scores || p.precisions || p.bp)
         warp_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, lane < N ? p.weights[lane] : 0.0,
                       p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
@@ -821,6 +826,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
           s_tot[2 * N] += static_cast<unsigned long long>(c);
           s_tot[2 * N + 1] += static_cast<unsigned long long>(r);
         }
+      }
       }
     }
     if (!dbuf && gi + gridDim.x < nb) {
