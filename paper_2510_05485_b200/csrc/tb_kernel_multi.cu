@@ -777,20 +777,23 @@ __global__ void __launch_bounds__(kMultiThreads, 2)
     __syncthreads();
     TB_MARK(24);
 
-    // ---- epilogue (warp 0)
+    // ---- epilogue: warp 0 the fp64 scores, warp 1 (in parallel) the integer outputs
+    if (tid >= 32 && tid < 64) {
+      const int64_t c = s_len[0];
+      if (lane < N) {
+        if (p.num) p.num[b * N + lane] = static_cast<int64_t>(s_hits[lane]);
+        if (p.den) p.den[b * N + lane] = c - lane > 0 ? c - lane : 0;
+      }
+      if (lane == 0) {
+        if (p.cand_len_out) p.cand_len_out[b] = c;
+        if (p.eff_ref) p.eff_ref[b] = s_effref;
+      }
+    }
     if (tid < 32) {
       const int64_t c = s_len[0];
       const int64_t num = lane < N ? static_cast<int64_t>(s_hits[lane]) : 0;
       const int64_t den = (lane < N && c - lane > 0) ? c - lane : 0;
-      if (lane < N) {
-        if (p.num) p.num[b * N + lane] = num;
-        if (p.den) p.den[b * N + lane] = den;
-      }
       const int64_t r = s_effref;
-      if (lane == 0) {
-        if (p.cand_len_out) p.cand_len_out[b] = c;
-        if (p.eff_ref) p.eff_ref[b] = r;
-      }
       if (p.scores || p.precisions || p.bp)
         warp_epilogue(num, den, c, r, N, p.smoothing, p.eps, p.k, lane < N ? p.weights[lane] : 0.0,
                       p.precisions ? p.precisions + b * N : nullptr, p.bp ? p.bp + b : nullptr,
