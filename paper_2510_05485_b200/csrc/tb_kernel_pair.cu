@@ -329,15 +329,39 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
             id1[pos] = static_cast<uint16_t>(leader);
             idn[pos] = static_cast<uint16_t>(leader);
           }
-          const unsigned lc = __ballot_sync(kFull, live && pos < roff);
-          const unsigned lr = __ballot_sync(kFull, live && pos >= roff);
-          const unsigned below = (1u << lane) - 1u;
-          if (live) lx[pos < roff ? __popc(lc & below) : roff + __popc(lr & below)] = static_cast<uint16_t>(pos);
           if (lane == 0) {
             s_hits[0] = h;
-            s_nc = __popc(lc);
-            s_nr = __popc(lr);
+            s_nc = 0;  // orders >= 2 are finished here: nothing left for the passes below
+            s_nr = 0;
           }
+          // orders 2..N of the same positions, still in this warp's registers
+          // (no block barrier, no list round trip): an n-gram's id for the
+          // next order is the lowest lane holding it
+          __syncwarp();  // the live positions' order-1 ids
+          int q0 = live ? pos : -1;
+          uint32_t pid = static_cast<uint32_t>(leader);
+          if (__any_sync(kFull, live && pos < roff))
+            for (int m = 2; m <= N; ++m) {
+              bool valid = q0 >= 0;
+              uint32_t key = 0;
+              if (valid) {
+                const int end = q0 < roff ? clen : roff + rlen;
+                const int q = q0 + m - 1;
+                valid = q < end && id1[q] != 0xffffu;
+                if (valid) key = (pid << 16) | id1[q];
+              }
+              const unsigned pm = __match_any_sync(kFull, valid ? key : 0xffffffffu - lane);
+              const unsigned cn = __popc(pm & __ballot_sync(kFull, valid && q0 < roff));
+              const unsigned xn = __popc(pm & __ballot_sync(kFull, valid && q0 >= roff));
+              const int ld = __ffs(pm) - 1;
+              unsigned hn = (valid && lane == ld) ? (cn < xn ? cn : xn) : 0u;
+              hn = __reduce_add_sync(kFull, hn);
+              if (lane == 0) s_hits[m - 1] = hn;
+              const bool ok = valid && (q0 < roff ? xn > 0 : cn > 0);
+              if (!__any_sync(kFull, ok && q0 < roff)) break;
+              q0 = ok ? q0 : -1;
+              pid = static_cast<uint32_t>(ld);
+            }
         }
       } else if (S <= kSmallSet) {
         filtered = true;  // the block compares the S listed tokens directly
