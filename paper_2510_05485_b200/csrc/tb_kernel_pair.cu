@@ -1,5 +1,5 @@
-// tb_kernel_pair.cu — single-reference kernel (R = 1), round-1 design
-// (see tb_common.cuh for the source layout, DESIGN.md §3 for the design)
+// tb_kernel_pair.cu — single-reference kernel (R = 1), the headline path
+// (see tb_common.cuh for the source layout, DESIGN.md §3.1 for the design)
 
 #include "tb_launch.cuh"
 
@@ -9,18 +9,22 @@ namespace {
 // --------------------------------------------------------------------------
 // Single-reference kernel (R == 1, the headline configuration).
 //
-// Order 1: a blocked two-bit Bloom filter per side (in the table + count
-// region) drops the tokens absent from the other side; when <= kSmallSet
-// positions survive (unrelated text) they are matched exactly without a
-// table.  Otherwise only CANDIDATE tokens are inserted, store-then-verify:
+// Order 1: a blocked two-bit Bloom filter (in the table + count region)
+// drops the tokens absent from the other side — two passes over both rows, or
+// (kThree, rows of more quads than threads) three: candidate tokens into Fc,
+// reference tokens against Fc, candidate tokens against the small filter of
+// the reference survivors.  When <= kSmallSet positions survive (unrelated
+// text) they are matched exactly without a table (<= 32: warp 0 with
+// match.any, which also finishes orders >= 2 in its registers).  Otherwise
+// only CANDIDATE tokens are inserted, store-then-verify:
 //   claim:  every candidate position stores itself (u16) into its token's
 //           home slot — plain stores, one wins;
 //   verify: the winner owns the slot (its own occurrence is counted
 //           implicitly); an equal token adds one to the owner's count word
-
-// NT threads per CTA: 256 (4 CTAs per SM) for batches of many groups, 512
-// (2 per SM) when the batch is one wave: every phase then has half the work per
-// thread, which is the per-group latency the step waits for.
+// and orders >= 2 run table rounds over the live lists.
+//
+// 256 threads per CTA (4 CTAs per SM); kList: the groups listed by the filter
+// kernel (tb_kernel_sparse.cu), which needed the hash passes.
 template <typename T, int NT, bool kList, bool kThree>
 __global__ void __launch_bounds__(NT, 1024 / NT)
     bleu_pair_kernel(const __grid_constant__ StatsParams p) {
@@ -179,7 +183,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
     // ================= order 1: filter =================
     // Each side marks its tokens in a blocked two-bit Bloom filter (the table
     // region: a 32-bit word per 4 slots per side, both bits of a token in one
-    // word); a token not in the other side's filter cannot match (false
+    // word; three-pass: the candidate side only, plus the small filter of the
+    // reference survivors); a token not in the other side's filter cannot match (false
     // positives ~0.1% at the table's load).  When at most kSmallSet positions pass (unrelated
     // text: the ~1% that match plus ~1% false positives), their tokens are
     // matched exactly among themselves — one warp with match.any up to 32, the
