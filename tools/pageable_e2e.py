@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2510_05485_b200 as tb  # noqa: E402
 
-b, l, v, r, sm = bench.WORKLOADS["c2"]
+b, l, v, r, sm = bench.WORKLOADS["c2"][:5]
 cfg = tb.BleuConfig(smoothing=sm)
 data = [bench.generate_batch(b, l, v, r, seed=42 + i) for i in range(8)]
 

@@ -4,7 +4,7 @@ time per step at large step counts (profiles/r01_experiments.md)."""
 import sys, time, torch
 sys.path.insert(0, '/root/repo')
 import bench, paper_2510_05485_b200 as tb
-b, l, v, r, sm = bench.WORKLOADS["c2"]
+b, l, v, r, sm = bench.WORKLOADS["c2"][:5]
 dev = torch.device("cuda", 0)
 plans = []
 gen = torch.Generator(device=dev)

@@ -13,7 +13,7 @@ import paper_2510_05485_b200 as tb  # noqa: E402
 
 
 def main(workload="c2"):
-    b, l, v, r, sm = bench.WORKLOADS[workload]
+    b, l, v, r, sm = bench.WORKLOADS[workload][:5]
     (cid, clen), refs = bench.generate_batch(b, l, v, r)
     cand = tb.TokenBatch(ids=torch.as_tensor(cid).cuda().to(torch.int32), lengths=torch.as_tensor(clen).cuda())
     rb = [tb.TokenBatch(ids=torch.as_tensor(i).cuda().to(torch.int32), lengths=torch.as_tensor(x).cuda())
