@@ -121,7 +121,8 @@ def config_dict(workload, data, world, scaling):
     return {"workload": f"{workload}: {'corpus' if mode == 'corpus' else 'per-sentence'} BLEU-4, "
                         f"B={b} L={l} V={v} R={r} smoothing={smoothing}, data={data}, "
                         + ("per GPU (weak scaling)" if scaling == "weak" else "one global batch (strong scaling)"),
-            "global_batch": gb, "seq_len": l, "parallelism": f"dp{world} (row shards)"}
+            "global_batch": gb, "seq_len": l, "parallelism": f"dp{world} (row shards)",
+            "l2": "inputs larger than L2: timed steps cycle distinct device-resident batches totalling >= 2x L2"}
 
 
 def shard_rows(b, world, rank):
