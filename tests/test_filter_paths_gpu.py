@@ -47,3 +47,29 @@ def test_filter_passes_around_the_switch(wc, wr, dtype):
     np.testing.assert_array_equal(st.numerators.cpu().numpy(), o["numerators"])
     np.testing.assert_array_equal(st.denominators.cpu().numpy(), o["denominators"])
     np.testing.assert_array_equal(st.eff_ref_lens.cpu().numpy(), o["eff_ref_lens"])
+
+
+@pytest.mark.parametrize("w", [200, 512, 1024])
+@pytest.mark.parametrize("n", [4, 9])
+def test_warp_path_long_shared_phrases(w, n):
+    """<= 32 survivors that form long shared n-grams: warp 0 finishes every
+    order in its registers right after the exact order-1 match."""
+    rng = np.random.default_rng(w * 31 + n)
+    b = 650
+    cid = rng.integers(0, 1 << 24, (b, w))
+    rid = rng.integers(0, 1 << 24, (b, w))
+    clen = rng.integers(w // 2, w + 1, b)
+    rlen = rng.integers(w // 2, w + 1, b)
+    for i in range(b):  # one or two phrases of up to 10 tokens copied into the reference
+        for _ in range(int(rng.integers(1, 3))):
+            k = int(rng.integers(1, 11))
+            s = int(rng.integers(0, clen[i] - k + 1))
+            d = int(rng.integers(0, rlen[i] - k + 1))
+            rid[i, d:d + k] = cid[i, s:s + k]
+    t = lambda a, dt=torch.int32: torch.as_tensor(a, dtype=dt, device="cuda")  # noqa: E731
+    cand = tb.TokenBatch(ids=t(cid), lengths=t(clen, torch.int64))
+    rb = [tb.TokenBatch(ids=t(rid), lengths=t(rlen, torch.int64))]
+    st = tb.compute_stats(cand, rb, tb.BleuConfig(max_order=n))
+    o = oracle.stats(cid, clen, [(rid, rlen)], n)
+    np.testing.assert_array_equal(st.numerators.cpu().numpy(), o["numerators"])
+    assert (o["numerators"][:, min(n, 5) - 1] > 0).any()  # long matches were exercised
