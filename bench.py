@@ -114,6 +114,20 @@ def moved_bytes(lengths_rows, b, n_out_words, token_bytes=4):
     return token_bytes * int(sum(int(x.sum()) for x in lens)) + 8 * b * len(lens) + 8 * n_out_words
 
 
+PCIE_GBS = 48.0  # pinned-host reads on this pool's B200 boxes (tools/microbench/pcie_read.cu)
+
+
+def pcie_roofline(leg, rows_per_step):
+    """The e2e path's own roofline: the host->device bytes of one step (valid
+    prefixes of this rank's rows) over the step time implied by the e2e rate,
+    against the measured PCIe read bandwidth."""
+    step_s = rows_per_step / leg["value"]
+    gbs = leg["h2d_bytes_per_step"] / step_s / 1e9
+    return {"achieved_gbs": gbs, "peak_gbs": PCIE_GBS, "frac": gbs / PCIE_GBS,
+            "peak_source": "measured: copy engine, 16-byte kernel loads and cp.async.bulk from pinned host "
+                           "memory all read 48-50 GB/s (profiles/r02_pcie_read.log)"}
+
+
 def config_dict(workload, data, world, scaling):
     """The `config` of a JSON line — identical in both arms."""
     b, l, v, r, smoothing, mode, _ = WORKLOADS[workload]
@@ -832,6 +846,7 @@ def run_ours(args):
                     "token_dtype": "int32",
                     "path": "sentence_bleu(TokenBatch(pinned int32 host tensors)) -> numpy: one blocking "
                             "tb_bleu_host call; the kernel streams valid row prefixes over PCIe",
+                    "pcie_roofline": pcie_roofline(e2e["pinned32"], m["rows_per_step"]),
                     "int64_tokens": e2e["pinned64"], "numpy_int64_tokens": e2e["numpy64"],
                     "fresh_numpy_int64": dict(e2e["fresh_numpy64"], path=(
                         "a NEW TokenBatch over numpy int64 arrays every step (construction + validation "
