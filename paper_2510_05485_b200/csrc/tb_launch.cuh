@@ -57,16 +57,18 @@ int launch_kernel(K kern, const StatsParams& prm, const Plan& pl, int sms, bool 
   if (persistent_fill) {
     // occupancy per (device, dynamic smem) of this kernel instantiation, cached:
     // the query costs microseconds on every launch otherwise
-    static thread_local struct { int dev; size_t smem; int occ; } cache[8] = {};
+    // (keyed by the kernel too: every stats kernel has the same C++ type)
+    static thread_local struct { const void* kern; int dev; size_t smem; int threads; int occ; } cache[16] = {};
     static thread_local int next = 0;
     int occ = 0;
+    const void* kp = reinterpret_cast<const void*>(kern);
     for (auto& e : cache)
-      if (e.occ > 0 && e.dev == dev && e.smem == pl.smem_bytes) occ = e.occ;
+      if (e.occ > 0 && e.kern == kp && e.dev == dev && e.smem == pl.smem_bytes && e.threads == threads) occ = e.occ;
     if (occ == 0) {
       TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, pl.smem_bytes));
       if (occ < 1) occ = 1;
-      cache[next] = {dev, pl.smem_bytes, occ};
-      next = (next + 1) & 7;
+      cache[next] = {kp, dev, pl.smem_bytes, threads, occ};
+      next = (next + 1) & 15;
     }
     const int64_t resident = static_cast<int64_t>(occ) * sms;
     grid = prm.batch < resident ? prm.batch : resident;
